@@ -1,0 +1,209 @@
+/*
+ * linoct_b200.h -- C ABI of the B200-native SFC reorder / linear octree / radius + kNN path.
+ *
+ * Drop-in boundary for the reference's C++ entry points (paths relative to
+ * /root/reference/proj).  Every entry point names the reference interface it replaces.
+ * Plain pointers and sizes only; no exceptions cross this boundary.  Host pointers are
+ * named `*_host`, device pointers `*_dev`.  Arrays of points are AoS xyz triples of f64
+ * (the layout of std::vector<linoct::Point>, geometry.hpp:14-20).
+ *
+ * Status codes mirror the reference's exception types:
+ *   LO_INVALID_ARGUMENT <-> std::invalid_argument, LO_DOMAIN_ERROR <-> std::domain_error,
+ *   LO_LOGIC_ERROR <-> std::logic_error.  lo_last_error() returns the message of the last
+ *   failure on the calling host thread.
+ */
+#ifndef LINOCT_B200_H
+#define LINOCT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LO_ABI_VERSION 1
+
+typedef enum {
+    LO_OK = 0,
+    LO_INVALID_ARGUMENT = 1,
+    LO_DOMAIN_ERROR = 2,
+    LO_LOGIC_ERROR = 3,
+    LO_OUT_OF_MEMORY = 4,
+    LO_CUDA_ERROR = 5,
+    LO_NO_DEVICE = 6
+} lo_status;
+
+/* enum class Curve {Morton, Hilbert} (sfc.hpp:17) */
+enum { LO_MORTON = 0, LO_HILBERT = 1 };
+/* enum class KernelShape {Sphere, Circle, Cube, Square} (geometry.hpp:101) */
+enum { LO_SPHERE = 0, LO_CIRCLE = 1, LO_CUBE = 2, LO_SQUARE = 3 };
+/* enum class RadiusMethod {Ptr, Lin, Prune, Struct} (search.hpp:108) */
+enum { LO_METHOD_PTR = 0, LO_METHOD_LIN = 1, LO_METHOD_PRUNE = 2, LO_METHOD_STRUCT = 3 };
+
+typedef struct lo_context lo_context; /* device, stream, memory pool, stage timers */
+typedef struct lo_coded lo_coded;     /* CodedCloud (reorder.hpp:14-20), device resident */
+typedef struct lo_octree lo_octree;   /* LinearOctree (linear_octree.hpp:40-118) */
+typedef struct lo_csr lo_csr;         /* BatchResult of run_radius_batch (search.hpp:121-131) */
+typedef struct lo_knn_result lo_knn_result;        /* BatchResult of run_knn_batch + the (index, dist) lists */
+
+/* LinearOctree::InternalNode, byte-identical (linear_octree.hpp:46-53; 56 bytes). */
+typedef struct {
+    uint64_t prefix;
+    int32_t children[8];
+    uint32_t begin;
+    uint32_t end;
+    uint8_t depth;
+    uint8_t child_mask;
+    uint8_t pad_[6];
+} lo_internal_node;
+
+typedef struct {
+    uint64_t n;           /* points */
+    int32_t curve;        /* LO_MORTON / LO_HILBERT */
+    int32_t level;        /* grid level, <= 21 */
+    double disc_box[6];   /* Discretizer bbox: cubified cloud bbox (reorder.cpp:71) */
+    double cloud_box[6];  /* PointCloud::bbox() of the input (geometry.hpp:74-81) */
+    double scale[3];      /* Discretizer scale per axis (sfc.cpp:77-80) */
+} lo_coded_info;
+
+typedef struct {
+    uint64_t leaves;      /* LeafArray::leaf_count() */
+    uint64_t internal;    /* internal_count() */
+    int32_t root;         /* root() NodeRef: >= 0 internal, < 0 is ~leaf */
+    uint32_t n_max;
+    int32_t level;
+    int32_t curve;
+    uint64_t points;
+    uint64_t tnodes;      /* traversal nodes (non-empty nodes), device side only */
+} lo_octree_info;
+
+typedef struct {
+    uint64_t rows;        /* centres */
+    uint64_t total;       /* neighbours over all rows (u64: cfg3 exceeds 2^32) */
+    double mean_count;    /* BatchResult::mean_count (mu) */
+    double device_ms;     /* device time of the batch (count + scan + fill [+ digests]) */
+} lo_csr_info;
+
+/* ---- context ------------------------------------------------------------------------ */
+const char* lo_last_error(void);
+int lo_abi_version(void);
+int lo_device_count(int* count);
+/* One context = one device + one CUDA stream.  stream = NULL creates a private stream;
+ * otherwise work is enqueued on the given cudaStream_t (e.g. torch's current stream). */
+int lo_context_create(int device, void* stream, lo_context** out);
+int lo_context_destroy(lo_context* ctx);
+int lo_context_synchronize(lo_context* ctx);
+void* lo_context_stream(lo_context* ctx);
+/* Per-stage device timers (CUDA events on the context stream); off by default. */
+int lo_context_set_timing(lo_context* ctx, int enabled);
+/* Copies up to cap (name, ms) pairs of the last timed operations; returns count. */
+int lo_context_stage_times(lo_context* ctx, char* names, int name_len, double* ms, int cap);
+/* Device buffers for harnesses (bench L2 flush, device-resident inputs). */
+int lo_device_alloc(lo_context* ctx, uint64_t bytes, void** out_dev);
+int lo_device_free(lo_context* ctx, void* dev);
+int lo_memcpy_h2d(lo_context* ctx, void* dst_dev, const void* src_host, uint64_t bytes);
+int lo_memcpy_d2h(lo_context* ctx, void* dst_host, const void* src_dev, uint64_t bytes);
+int lo_host_alloc_pinned(uint64_t bytes, void** out_host);
+int lo_host_free_pinned(void* host);
+/* Writes `bytes` of a scratch buffer (L2 flush between timed iterations). */
+int lo_flush_l2(lo_context* ctx, void* scratch_dev, uint64_t bytes);
+
+/* ---- sfc (sfc.hpp:56-83, sfc.cpp:8-73) -------------------------------------------- */
+/* Per-point codes in cloud order; replaces compute_codes(cloud, curve) (reorder.hpp:28)
+ * and, with disc_box != NULL, compute_codes(cloud, curve, disc) (reorder.hpp:23). */
+int lo_compute_codes(lo_context* ctx, const double* xyz_host, uint64_t n, int curve, int level,
+                     const double* disc_box /* NULL = cubify(bbox) */, uint64_t* codes_host);
+/* Bulk codecs on grid cells (morton_/hilbert_encode, sfc_decode). */
+int lo_encode_cells(lo_context* ctx, const uint32_t* cells_host, uint64_t n, int curve,
+                    int level, uint64_t* codes_host);
+int lo_decode_codes(lo_context* ctx, const uint64_t* codes_host, uint64_t n, int curve,
+                    int level, uint32_t* cells_host);
+
+/* ---- reorder (reorder.cpp:66-89) ---------------------------------------------------- */
+/* reorder_cloud(cloud, curve, level) -> CodedCloud.  Host input (H2D inside). */
+int lo_reorder(lo_context* ctx, const double* xyz_host, uint64_t n, int curve, int level,
+               lo_coded** out);
+/* Same with the cloud already resident in device memory (AoS f64, n*3). */
+int lo_reorder_device(lo_context* ctx, const double* xyz_dev, uint64_t n, int curve, int level,
+                      lo_coded** out);
+int lo_coded_info_get(const lo_coded* coded, lo_coded_info* out);
+/* Download the reordered cloud (AoS), sorted codes and permutation[new] = old; any NULL
+ * pointer is skipped. */
+int lo_coded_download(lo_context* ctx, const lo_coded* coded, double* xyz_host,
+                      uint64_t* codes_host, uint32_t* perm_host);
+/* Device pointers of the SoA sorted coordinates / codes / permutation (read only). */
+int lo_coded_device_ptrs(const lo_coded* coded, const double** x, const double** y,
+                         const double** z, const uint64_t** codes, const uint32_t** perm);
+int lo_coded_destroy(lo_coded* coded);
+/* invert_permutation (reorder.hpp:36) */
+int lo_invert_permutation(lo_context* ctx, const uint32_t* perm_host, uint64_t n,
+                          uint32_t* inv_host);
+
+/* ---- linear octree (linear_octree.cpp:23-147) --------------------------------------- */
+/* build_leaves(codes, n_max, level, threads) (linear_octree.hpp:33-34); sorted codes in,
+ * LeafArray out.  Size query: boundaries_host == NULL returns *leaves only. */
+int lo_build_leaves(lo_context* ctx, const uint64_t* codes_host, uint64_t n, uint32_t n_max,
+                    int level, uint64_t* leaves, uint64_t* boundaries_host,
+                    uint32_t* offsets_host, uint64_t cap);
+/* LinearOctree(coded, n_max, threads) (linear_octree.hpp:55).  `threads` is ignored. */
+int lo_octree_build(lo_context* ctx, const lo_coded* coded, uint32_t n_max, lo_octree** out);
+int lo_octree_info_get(const lo_octree* tree, lo_octree_info* out);
+/* leaves() boundaries[L+1], offsets[L+1]; internal_nodes() [I]; NULL skips. */
+int lo_octree_download(lo_context* ctx, const lo_octree* tree, uint64_t* boundaries_host,
+                       uint32_t* offsets_host, lo_internal_node* nodes_host);
+/* node_bounds(ref) (linear_octree.cpp:139-147) for a batch of NodeRefs: 6 f64 per ref. */
+int lo_octree_node_bounds(lo_context* ctx, const lo_octree* tree, const int32_t* refs_host,
+                          uint64_t count, double* boxes_host);
+int lo_octree_destroy(lo_octree* tree);
+
+/* ---- radius search (search.cpp:45-156, :261-351) ------------------------------------ */
+/* run_radius_batch(tree, coded, method, shape, radius, options).  centres_host == NULL is
+ * BatchMode::Full (every point, in sorted order); otherwise `m` cloud indices.  The CSR
+ * (u64 row offsets, u32 ascending indices) stays on the device until downloaded. */
+int lo_radius(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int method,
+              int shape, double radius, const uint32_t* centres_host, uint64_t m,
+              int fingerprint, lo_csr** out);
+/* Same with explicit query points (neighbours_lin(tree, coded, SearchKernel) at arbitrary
+ * centres, search.hpp:61-64): queries_host is AoS f64, m*3. */
+int lo_radius_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int shape,
+                     double radius, const double* queries_host, uint64_t m, lo_csr** out);
+int lo_csr_info_get(const lo_csr* csr, lo_csr_info* out);
+/* counts[m], fingerprints[m] (FNV-1a-64, search.cpp:263-271), offsets[m+1], indices[total]. */
+int lo_csr_download(lo_context* ctx, const lo_csr* csr, uint32_t* counts_host,
+                    uint64_t* fingerprints_host, uint64_t* offsets_host, uint32_t* indices_host);
+int lo_csr_device_ptrs(const lo_csr* csr, const uint64_t** offsets, const uint32_t** indices);
+int lo_csr_destroy(lo_csr* csr);
+
+/* ---- kNN (search.cpp:158-259, :369-388) --------------------------------------------- */
+/* run_knn_batch(tree, coded, k, options): per row min(k, N) (index, dist_sq) ascending by
+ * (dist_sq, index).  k < 1 -> LO_INVALID_ARGUMENT. */
+int lo_knn(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32_t k,
+           const uint32_t* centres_host, uint64_t m, int fingerprint, lo_knn_result** out);
+/* knn_lin_oct(tree, coded, Point, k) at arbitrary centres (search.hpp:101-105). */
+int lo_knn_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32_t k,
+                  const double* queries_host, uint64_t m, lo_knn_result** out);
+/* rows, k_eff (= min(k, N)), device ms */
+int lo_knn_info_get(const lo_knn_result* res, uint64_t* rows, uint32_t* k_eff, double* device_ms);
+/* idx[m*k_eff], dist[m*k_eff], fingerprints[m]; NULL skips. */
+int lo_knn_download(lo_context* ctx, const lo_knn_result* res, uint32_t* idx_host, double* dist_host,
+                    uint64_t* fingerprints_host);
+int lo_knn_destroy(lo_knn_result* res);
+
+/* ---- locality histogram (locality.cpp:41-97), log2 bins ----------------------------- */
+/* bins[b]: count of |map(i) - map(j)| over kNN pairs with b = 0 for d = 0 and
+ * floor(log2 d) + 1 otherwise (33 bins).  use_perm = 1 maps through the permutation. */
+int lo_locality_log2(lo_context* ctx, const lo_knn_result* res, const lo_coded* coded,
+                     const uint32_t* centres_host, int use_perm, uint64_t* bins33_host);
+
+/* ---- synthetic clouds (host; io.cpp:122-130 and SURVEY.md §8d) ---------------------- */
+int lo_generate_uniform(uint64_t n, uint64_t seed, double extent, double* xyz_host);
+int lo_generate_terrain(uint64_t n, uint64_t seed, double extent_xy, double* xyz_host);
+int lo_generate_mixed(uint64_t n, uint64_t seed, double* xyz_host);
+/* sample_indices(n, k, seed) (rng.hpp:46-58) */
+int lo_sample_indices(uint32_t n, uint32_t k, uint64_t seed, uint32_t* out_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LINOCT_B200_H */

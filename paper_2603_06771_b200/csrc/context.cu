@@ -1,0 +1,421 @@
+// context.cu -- contexts, errors, device memory, stage timers, exclusive scans, host tables.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+
+#include "lo_internal.cuh"
+
+namespace lo {
+
+thread_local std::string g_last_error;
+void set_last_error(const char* m) { g_last_error = m; }
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+                  cudaGetErrorString(e), what, file, line);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();  // clear the sticky-free allocation error
+        throw Error(LO_OUT_OF_MEMORY, buf);
+    }
+    throw Error(LO_CUDA_ERROR, buf);
+}
+
+void* dalloc(lo_context* ctx, size_t bytes) {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes, ctx->stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        char buf[160];
+        std::snprintf(buf, sizeof buf, "device allocation of %zu bytes failed (%s)", bytes,
+                      cudaGetErrorName(e));
+        throw Error(LO_OUT_OF_MEMORY, buf);
+    }
+    return p;
+}
+
+void dfree(lo_context* ctx, void* p) {
+    if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+void sync(lo_context* ctx) { LO_CUDA(cudaStreamSynchronize(ctx->stream)); }
+
+void stage_begin(lo_context* ctx, const char* name) {
+    if (!ctx->timing) return;
+    lo_context::Stage s{name, nullptr, nullptr};
+    LO_CUDA(cudaEventCreate(&s.a));
+    LO_CUDA(cudaEventCreate(&s.b));
+    LO_CUDA(cudaEventRecord(s.a, ctx->stream));
+    ctx->stages.push_back(s);
+}
+
+void stage_end(lo_context* ctx) {
+    if (!ctx->timing || ctx->stages.empty()) return;
+    LO_CUDA(cudaEventRecord(ctx->stages.back().b, ctx->stream));
+}
+
+static void resolve_stages(lo_context* ctx) {
+    if (ctx->stages.empty()) return;
+    sync(ctx);
+    for (auto& s : ctx->stages) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, s.a, s.b);
+        ctx->stage_ms.emplace_back(s.name, ms);
+        cudaEventDestroy(s.a);
+        cudaEventDestroy(s.b);
+    }
+    ctx->stages.clear();
+}
+
+// ---- exclusive scan (3 phases: tile sums, scan of sums, tile scans) ----------------------
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+template <class In>
+__global__ void __launch_bounds__(kScanThreads) scan_tile_sums(const In* in, u64 n, u64* sums) {
+    using BlockReduce = cub::BlockReduce<u64, kScanThreads>;
+    __shared__ typename BlockReduce::TempStorage tmp;
+    const u64 base = static_cast<u64>(blockIdx.x) * kScanTile;
+    u64 acc = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        const u64 j = base + static_cast<u64>(i) * kScanThreads + threadIdx.x;
+        if (j < n) acc += in[j];
+    }
+    const u64 s = BlockReduce(tmp).Sum(acc);
+    if (threadIdx.x == 0) sums[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(1024) scan_sums(u64* sums, int nb, u64* total_out) {
+    using BlockScan = cub::BlockScan<u64, 1024>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    __shared__ u64 carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nb; base += 1024) {
+        const int j = base + threadIdx.x;
+        const u64 v = j < nb ? sums[j] : 0;
+        u64 ex, agg;
+        BlockScan(tmp).ExclusiveSum(v, ex, agg);
+        if (j < nb) sums[j] = ex + carry;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += agg;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total_out = carry;
+}
+
+template <class In, class Out>
+__global__ void __launch_bounds__(kScanThreads) scan_tiles(const In* in, u64 n, const u64* sums,
+                                                           Out* out) {
+    using BlockScan = cub::BlockScan<u64, kScanThreads>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    __shared__ __align__(16) unsigned char raw[kScanTile * sizeof(Out) > kScanTile * sizeof(In)
+                                                   ? kScanTile * sizeof(Out)
+                                                   : kScanTile * sizeof(In)];
+    In* tile = reinterpret_cast<In*>(raw);
+    Out* otile = reinterpret_cast<Out*>(raw);
+    const u64 base = static_cast<u64>(blockIdx.x) * kScanTile;
+    // coalesced load into shared memory, then each thread scans a blocked run
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        const int t = i * kScanThreads + threadIdx.x;
+        const u64 j = base + t;
+        tile[t] = j < n ? in[j] : In(0);
+    }
+    __syncthreads();
+    u64 run = 0;
+    In v[kScanItems];
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        v[i] = tile[threadIdx.x * kScanItems + i];
+        run += v[i];
+    }
+    u64 ex;
+    BlockScan(tmp).ExclusiveSum(run, ex);
+    ex += sums[blockIdx.x];
+    __syncthreads();
+    // write back through shared memory in the output type for coalesced stores
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        otile[threadIdx.x * kScanItems + i] = static_cast<Out>(ex);
+        ex += v[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        const int t = i * kScanThreads + threadIdx.x;
+        const u64 j = base + t;
+        if (j < n) out[j] = otile[t];
+    }
+}
+
+template <class Out>
+__global__ void store_total(const u64* s, Out* o) { *o = static_cast<Out>(*s); }
+
+template <class In, class Out>
+static void exclusive_scan(lo_context* ctx, const In* in, Out* out, u64 n) {
+    const int nb = std::max(1, ceil_div(n, kScanTile));
+    u64* sums = dalloc_t<u64>(ctx, nb + 1);
+    if (n > 0) {
+        scan_tile_sums<In><<<nb, kScanThreads, 0, ctx->stream>>>(in, n, sums);
+        LO_CHECK_LAUNCH();
+    } else {
+        LO_CUDA(cudaMemsetAsync(sums, 0, sizeof(u64), ctx->stream));
+    }
+    scan_sums<<<1, 1024, 0, ctx->stream>>>(sums, n > 0 ? nb : 1, sums + nb);
+    LO_CHECK_LAUNCH();
+    if (n > 0) {
+        scan_tiles<In, Out><<<nb, kScanThreads, 0, ctx->stream>>>(in, n, sums, out);
+        LO_CHECK_LAUNCH();
+    }
+    // out[n] = total
+    store_total<Out><<<1, 1, 0, ctx->stream>>>(sums + nb, out + n);
+    LO_CHECK_LAUNCH();
+    dfree(ctx, sums);
+}
+
+void exclusive_scan_u32_to_u64(lo_context* ctx, const u32* in, u64* out, u64 n) {
+    exclusive_scan<u32, u64>(ctx, in, out, n);
+}
+void exclusive_scan_u32(lo_context* ctx, const u32* in, u32* out, u64 n) {
+    exclusive_scan<u32, u32>(ctx, in, out, n);
+}
+
+// ---- curve tables ------------------------------------------------------------------------
+// Host Skilling decode (the transpose-to-axes half of the published Hilbert construction the
+// reference uses, sfc.cpp:44-73); only used here to derive the descent tables.
+static void hilbert_decode_host(u64 code, int level, u32 out[3]) {
+    if (level == 0) {
+        out[0] = out[1] = out[2] = 0;
+        return;
+    }
+    const u32 mask = (1u << level) - 1;
+    u32 a[3] = {compact3(code >> 2) & mask, compact3(code >> 1) & mask, compact3(code) & mask};
+    const u32 t = a[2] >> 1;
+    a[2] ^= a[1];
+    a[1] ^= a[0];
+    a[0] ^= t;
+    for (u32 q = 2; q != (2u << (level - 1)); q <<= 1) {
+        const u32 low = q - 1;
+        for (int i = 2; i >= 0; --i) {
+            if (a[i] & q) {
+                a[0] ^= low;
+            } else {
+                const u32 s = (a[0] ^ a[i]) & low;
+                a[0] ^= s;
+                a[i] ^= s;
+            }
+        }
+    }
+    out[0] = a[0], out[1] = a[1], out[2] = a[2];
+}
+
+static void decode_host(int curve, u64 code, int level, u32 out[3]) {
+    if (curve == LO_MORTON) {
+        out[0] = compact3(code >> 2), out[1] = compact3(code >> 1), out[2] = compact3(code);
+    } else {
+        hilbert_decode_host(code, level, out);
+    }
+}
+
+// Closure of child-digit signatures reachable from the root (same construction as
+// CurveStepper, sfc.cpp:157-194), verified by re-decoding every level-5 code.
+static CurveTables derive_tables(int curve) {
+    CurveTables t{};
+    std::vector<u32> sig;
+    std::vector<std::pair<u64, int>> ex;
+    auto signature = [&](u64 prefix, int depth) {
+        u32 s = 0;
+        for (int c = 0; c < 8; ++c) {
+            u32 cell[3];
+            decode_host(curve, prefix * 8 + c, depth + 1, cell);
+            s |= (((cell[0] & 1u) << 2) | ((cell[1] & 1u) << 1) | (cell[2] & 1u)) << (3 * c);
+        }
+        return s;
+    };
+    auto state_of = [&](u64 prefix, int depth) {
+        const u32 s = signature(prefix, depth);
+        for (size_t i = 0; i < sig.size(); ++i)
+            if (sig[i] == s) return static_cast<int>(i);
+        sig.push_back(s);
+        ex.emplace_back(prefix, depth);
+        require(sig.size() <= 32, LO_LOGIC_ERROR, "curve tables: state set does not close");
+        return static_cast<int>(sig.size() - 1);
+    };
+    state_of(0, 0);
+    for (size_t s = 0; s < sig.size(); ++s) {
+        for (int c = 0; c < 8; ++c) {
+            const int g = (sig[s] >> (3 * c)) & 7;
+            const int nx = state_of(ex[s].first * 8 + c, ex[s].second + 1);
+            t.dec[s * 8 + c] = static_cast<u8>(g | (nx << 3));
+            t.enc[s * 8 + g] = static_cast<u8>(c | (nx << 3));
+        }
+    }
+    t.states = static_cast<int>(sig.size());
+    for (int level = 1; level <= 5; ++level) {
+        for (u64 code = 0; code < (1ull << (3 * level)); ++code) {
+            int s = 0;
+            u32 w[3] = {0, 0, 0};
+            for (int d = level - 1; d >= 0; --d) {
+                const u8 e = t.dec[s * 8 + ((code >> (3 * d)) & 7)];
+                w[0] = w[0] << 1 | ((e >> 2) & 1);
+                w[1] = w[1] << 1 | ((e >> 1) & 1);
+                w[2] = w[2] << 1 | (e & 1);
+                s = e >> 3;
+            }
+            u32 ref[3];
+            decode_host(curve, code, level, ref);
+            require(w[0] == ref[0] && w[1] == ref[1] && w[2] == ref[2], LO_LOGIC_ERROR,
+                    "curve tables disagree with the decoder");
+        }
+    }
+    return t;
+}
+
+const CurveTables& curve_tables(int curve) {
+    static std::once_flag once;
+    static CurveTables tables[2];
+    std::call_once(once, [] {
+        tables[0] = derive_tables(LO_MORTON);
+        tables[1] = derive_tables(LO_HILBERT);
+    });
+    return tables[curve == LO_MORTON ? 0 : 1];
+}
+
+}  // namespace lo
+
+using namespace lo;
+
+// ---- C ABI: context -----------------------------------------------------------------------
+extern "C" {
+
+const char* lo_last_error(void) { return g_last_error.c_str(); }
+int lo_abi_version(void) { return LO_ABI_VERSION; }
+
+int lo_device_count(int* count) {
+    return api([&] {
+        int c = 0;
+        cudaError_t e = cudaGetDeviceCount(&c);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            c = 0;
+        }
+        *count = c;
+    });
+}
+
+int lo_context_create(int device, void* stream, lo_context** out) {
+    return api([&] {
+        int count = 0;
+        cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0) {
+            cudaGetLastError();
+            throw Error(LO_NO_DEVICE, "no CUDA device available: the B200 path has no CPU "
+                                      "fallback");
+        }
+        require(device >= 0 && device < count, LO_INVALID_ARGUMENT, "device index out of range");
+        LO_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        LO_CUDA(cudaGetDeviceProperties(&prop, device));
+        require(prop.major >= 10, LO_NO_DEVICE,
+                "device is not sm_100 class (this library is built for sm_100a only)");
+        auto* ctx = new lo_context;
+        ctx->device = device;
+        ctx->sm_count = prop.multiProcessorCount;
+        if (stream) {
+            ctx->stream = static_cast<cudaStream_t>(stream);
+        } else {
+            LO_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+            ctx->own_stream = true;
+        }
+        cudaMemPool_t pool;
+        LO_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        u64 threshold = ~0ull;
+        LO_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+        LO_CUDA(cudaMallocHost(&ctx->pinned_scratch, 4096));
+        curve_tables(LO_HILBERT);  // derive + self-check once
+        *out = ctx;
+    });
+}
+
+int lo_context_destroy(lo_context* ctx) {
+    return api([&] {
+        if (!ctx) return;
+        cudaStreamSynchronize(ctx->stream);
+        for (auto& s : ctx->stages) {
+            cudaEventDestroy(s.a);
+            cudaEventDestroy(s.b);
+        }
+        if (ctx->pinned_scratch) cudaFreeHost(ctx->pinned_scratch);
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int lo_context_synchronize(lo_context* ctx) { return api([&] { sync(ctx); }); }
+void* lo_context_stream(lo_context* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int lo_context_set_timing(lo_context* ctx, int enabled) {
+    return api([&] {
+        ctx->timing = enabled != 0;
+        ctx->stage_ms.clear();
+    });
+}
+
+int lo_context_stage_times(lo_context* ctx, char* names, int name_len, double* ms, int cap) {
+    int n = 0;
+    const int rc = api([&] {
+        resolve_stages(ctx);
+        for (auto& [name, t] : ctx->stage_ms) {
+            if (n >= cap) break;
+            if (names && name_len > 0) {
+                std::strncpy(names + static_cast<size_t>(n) * name_len, name.c_str(), name_len - 1);
+                names[static_cast<size_t>(n) * name_len + name_len - 1] = 0;
+            }
+            if (ms) ms[n] = t;
+            ++n;
+        }
+        ctx->stage_ms.clear();
+    });
+    return rc == LO_OK ? n : -rc;
+}
+
+int lo_device_alloc(lo_context* ctx, uint64_t bytes, void** out_dev) {
+    return api([&] {
+        *out_dev = dalloc(ctx, bytes);
+        sync(ctx);
+    });
+}
+int lo_device_free(lo_context* ctx, void* dev) {
+    return api([&] {
+        dfree(ctx, dev);
+        sync(ctx);
+    });
+}
+int lo_memcpy_h2d(lo_context* ctx, void* dst, const void* src, uint64_t bytes) {
+    return api([&] {
+        LO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        sync(ctx);
+    });
+}
+int lo_memcpy_d2h(lo_context* ctx, void* dst, const void* src, uint64_t bytes) {
+    return api([&] {
+        LO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+    });
+}
+int lo_host_alloc_pinned(uint64_t bytes, void** out_host) {
+    return api([&] { LO_CUDA(cudaMallocHost(out_host, bytes)); });
+}
+int lo_host_free_pinned(void* host) { return api([&] { LO_CUDA(cudaFreeHost(host)); }); }
+
+int lo_flush_l2(lo_context* ctx, void* scratch, uint64_t bytes) {
+    return api([&] { LO_CUDA(cudaMemsetAsync(scratch, 0x5a, bytes, ctx->stream)); });
+}
+
+}  // extern "C"

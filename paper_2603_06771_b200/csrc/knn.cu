@@ -1,0 +1,415 @@
+// knn.cu -- K7 exact kNN over the octree, K8 kNN row digests, K9 locality histogram.
+//
+// Replaces knn_lin_oct / run_knn_batch (search.cpp:158-259, :369-388) and the locality
+// accumulation (locality.cpp:41-97).  The reference's best-first queue emits the first k
+// points of the whole cloud under the order (dist_sq, index); this kernel computes the same
+// set with a warp-shared depth-first walk: one warp owns 32 consecutive queries, children are
+// visited nearest-first (distance from the tile's mean query to the child's box), and each
+// lane keeps a bounded max-heap of its k best (dist_sq, index) pairs.  A lane skips a node
+// only when its heap is full and the box's lower bound is strictly greater than its current
+// worst distance, so equal-distance points with a lower index are never lost.
+#include <algorithm>
+#include <cmath>
+
+#include "search_common.cuh"
+
+namespace lo {
+
+u32* upload_centres(lo_context* ctx, const u32* centres_host, u64 m, u64 n);
+void upload_points(lo_context* ctx, const double* xyz_host, u64 m, double** x, double** y,
+                   double** z);
+
+// (a.d, a.i) > (b.d, b.i) lexicographically: heap_after (search.cpp:173-177) on points.
+__device__ __forceinline__ bool after(double ad, u32 ai, double bd, u32 bi) {
+    return ad > bd || (ad == bd && ai > bi);
+}
+
+// Max-heap of one lane; element e lives at hd[e * 32] / hi[e * 32] (lane-interleaved).
+struct LaneHeap {
+    double* hd;
+    u32* hi;
+    u32 size;
+
+    __device__ __forceinline__ void push(double d, u32 i) {
+        u32 pos = size++;
+        while (pos > 0) {
+            const u32 par = (pos - 1) >> 1;
+            const double pd = hd[par * 32];
+            const u32 pi = hi[par * 32];
+            if (!after(d, i, pd, pi)) break;
+            hd[pos * 32] = pd;
+            hi[pos * 32] = pi;
+            pos = par;
+        }
+        hd[pos * 32] = d;
+        hi[pos * 32] = i;
+    }
+
+    // replace the maximum and restore the heap over [0, n)
+    __device__ __forceinline__ void sift_down(double d, u32 i, u32 n) {
+        u32 pos = 0;
+        for (;;) {
+            u32 c = 2 * pos + 1;
+            if (c >= n) break;
+            double cd = hd[c * 32];
+            u32 ci = hi[c * 32];
+            if (c + 1 < n) {
+                const double rd = hd[(c + 1) * 32];
+                const u32 ri = hi[(c + 1) * 32];
+                if (after(rd, ri, cd, ci)) {
+                    c = c + 1;
+                    cd = rd;
+                    ci = ri;
+                }
+            }
+            if (!after(cd, ci, d, i)) break;
+            hd[pos * 32] = cd;
+            hi[pos * 32] = ci;
+            pos = c;
+        }
+        hd[pos * 32] = d;
+        hi[pos * 32] = i;
+    }
+};
+
+constexpr int kKnnSmemBudget = 200 * 1024;
+
+template <bool GLOBAL_HEAP>
+__global__ void __launch_bounds__(128) knn_kernel(const TNode* __restrict__ tn,
+                                                  const double* __restrict__ px,
+                                                  const double* __restrict__ py,
+                                                  const double* __restrict__ pz, Queries q, u32 k,
+                                                  u32 keff, u32* __restrict__ out_idx,
+                                                  double* __restrict__ out_dist,
+                                                  double* __restrict__ gheap_d,
+                                                  u32* __restrict__ gheap_i) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warps = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // shared layout: [stack: warps * kStackCap u32][sx, sy, sz: warps * 32 f64 each][heaps]
+    u32* stack = reinterpret_cast<u32*>(smem) + w * kStackCap;
+    double* stage = reinterpret_cast<double*>(smem + sizeof(u32) * kStackCap * warps);
+    double* sx = stage + w * 96;
+    double* sy = sx + 32;
+    double* sz = sy + 32;
+    double* hd;
+    u32* hi;
+    if (GLOBAL_HEAP) {
+        const u64 slot = static_cast<u64>(blockIdx.x) * warps + w;
+        hd = gheap_d + slot * k * 32 + lane;
+        hi = gheap_i + slot * k * 32 + lane;
+    } else {
+        double* heaps_d = stage + warps * 96;
+        u32* heaps_i = reinterpret_cast<u32*>(heaps_d + static_cast<u64>(warps) * k * 32);
+        hd = heaps_d + static_cast<u64>(w) * k * 32 + lane;
+        hi = heaps_i + static_cast<u64>(w) * k * 32 + lane;
+    }
+    const u64 ntiles = (q.m + 31) / 32;
+    for (u64 tile = static_cast<u64>(blockIdx.x) * warps + w; tile < ntiles;
+         tile += static_cast<u64>(gridDim.x) * warps) {
+        const u64 qi = tile * 32 + lane;
+        const bool active = qi < q.m;
+        double cx = 0.0, cy = 0.0, cz = 0.0;
+        if (active) load_query(q, qi, cx, cy, cz);
+        // warp anchor for the child visiting order: mean of the active queries
+        double ax = active ? cx : 0.0, ay = active ? cy : 0.0, az = active ? cz : 0.0;
+        const int nact = __popc(__ballot_sync(~0u, active));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ax += __shfl_xor_sync(~0u, ax, o);
+            ay += __shfl_xor_sync(~0u, ay, o);
+            az += __shfl_xor_sync(~0u, az, o);
+        }
+        ax /= nact, ay /= nact, az /= nact;
+        LaneHeap heap{hd, hi, 0};
+        double worst_d = 0.0;
+        u32 worst_i = 0;
+        int sp = 1;
+        if (lane == 0) stack[0] = 0;
+        __syncwarp();
+        while (sp > 0) {
+            const u32 t = stack[--sp];
+            const NodeView nd = load_node(tn, t);
+            bool visit = false;
+            if (active) visit = heap.size < k || box_dist_sq(cx, cy, cz, nd) <= worst_d;
+            if (!__any_sync(~0u, visit)) continue;
+            if (nd.nchild == 0) {
+                for (u32 base = nd.begin; base < nd.end; base += 32) {
+                    const u32 j = base + lane;
+                    __syncwarp();
+                    if (j < nd.end) {
+                        sx[lane] = px[j];
+                        sy[lane] = py[j];
+                        sz[lane] = pz[j];
+                    }
+                    __syncwarp();
+                    if (visit) {
+                        const u32 cnt = min(32u, nd.end - base);
+                        for (u32 jj = 0; jj < cnt; ++jj) {
+                            const double d = point_dist_sq(sx[jj], sy[jj], sz[jj], cx, cy, cz);
+                            const u32 id = base + jj;
+                            if (heap.size < k) {
+                                heap.push(d, id);
+                                if (heap.size == k) {
+                                    worst_d = hd[0];
+                                    worst_i = hi[0];
+                                }
+                            } else if (after(worst_d, worst_i, d, id)) {
+                                heap.sift_down(d, id, k);
+                                worst_d = hd[0];
+                                worst_i = hi[0];
+                            }
+                        }
+                    }
+                }
+            } else {
+                // nearest-first: rank children by (box distance to the anchor, code order)
+                double cd = 0.0;
+                const u32 nc = nd.nchild;
+                if (lane < static_cast<int>(nc)) cd = box_dist_sq(ax, ay, az, load_node(tn, nd.child0 + lane));
+                u32 rank = 0;
+                for (u32 o = 0; o < nc; ++o) {
+                    const double od = __shfl_sync(~0u, cd, o);
+                    if (od < cd || (od == cd && static_cast<int>(o) < lane)) ++rank;
+                }
+                __syncwarp();
+                if (lane < static_cast<int>(nc)) stack[sp + nc - 1 - rank] = nd.child0 + lane;
+                sp += nc;
+                __syncwarp();
+            }
+        }
+        if (active) {
+            // heap sort in place -> ascending (dist_sq, index), then write the row
+            const u32 n = heap.size;
+            for (u32 e = n; e > 1; --e) {
+                const double td = hd[0];
+                const u32 ti = hi[0];
+                const double ld = hd[(e - 1) * 32];
+                const u32 li = hi[(e - 1) * 32];
+                hd[(e - 1) * 32] = td;
+                hi[(e - 1) * 32] = ti;
+                heap.sift_down(ld, li, e - 1);
+            }
+            u32* oi = out_idx + qi * keff;
+            double* od = out_dist + qi * keff;
+            for (u32 e = 0; e < n; ++e) {
+                oi[e] = hi[e * 32];
+                od[e] = hd[e * 32];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// FNV-1a-64 of (index, bit pattern of dist_sq) pairs (search.cpp:376-381).
+__global__ void knn_digest(const u32* __restrict__ idx, const double* __restrict__ dist, u64 m,
+                           u32 keff, u64* __restrict__ fps) {
+    for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < m;
+         r += (u64)gridDim.x * blockDim.x) {
+        u64 h = kFnvOffset;
+        for (u32 j = 0; j < keff; ++j) {
+            h = fnv_u32(h, idx[r * keff + j]);
+            h = fnv_u64(h, static_cast<u64>(__double_as_longlong(dist[r * keff + j])));
+        }
+        fps[r] = h;
+    }
+}
+
+// K9: log2-binned |map(i) - map(j)| over every (centre, neighbour) pair (locality.cpp:41-87).
+__global__ void locality_kernel(const u32* __restrict__ idx, u64 m, u32 keff,
+                                const u32* __restrict__ centres, const u32* __restrict__ map,
+                                unsigned long long* __restrict__ bins) {
+    __shared__ unsigned long long sb[33];
+    if (threadIdx.x < 33) sb[threadIdx.x] = 0;
+    __syncthreads();
+    for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < m * keff;
+         e += (u64)gridDim.x * blockDim.x) {
+        const u64 r = e / keff;
+        const u32 ci = centres ? centres[r] : static_cast<u32>(r);
+        const u64 mi = map ? map[ci] : ci;
+        const u64 mj = map ? map[idx[e]] : idx[e];
+        const u64 d = mi > mj ? mi - mj : mj - mi;
+        const int b = d == 0 ? 0 : 64 - __clzll(static_cast<long long>(d));
+        atomicAdd(&sb[b], 1ull);
+    }
+    __syncthreads();
+    if (threadIdx.x < 33 && sb[threadIdx.x]) atomicAdd(&bins[threadIdx.x], sb[threadIdx.x]);
+}
+
+static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_coded* c, u32 k,
+                                 const Queries& q, bool fingerprint) {
+    require(t != nullptr && c != nullptr, LO_INVALID_ARGUMENT, "null tree or cloud");
+    require(k >= 1, LO_INVALID_ARGUMENT, "knn: k must be >= 1");
+    auto* out = new lo_knn_result;
+    out->ctx = ctx;
+    out->rows = q.m;
+    out->k = k;
+    out->keff = static_cast<u32>(std::min<u64>(k, c->n));
+    // the heap never holds more than N entries, so k > N behaves as k = N
+    const u32 kh = out->keff;
+    cudaEvent_t e0, e1;
+    LO_CUDA(cudaEventCreate(&e0));
+    LO_CUDA(cudaEventCreate(&e1));
+    double* gd = nullptr;
+    u32* gi = nullptr;
+    try {
+        LO_CUDA(cudaEventRecord(e0, ctx->stream));
+        out->idx = dalloc_t<u32>(ctx, q.m * kh);
+        out->dist = dalloc_t<double>(ctx, q.m * kh);
+        const size_t per_warp_heap = static_cast<size_t>(kh) * 32 * 12;
+        const size_t per_warp_fixed = sizeof(u32) * kStackCap + 96 * sizeof(double);
+        const bool global_heap = per_warp_heap + per_warp_fixed > static_cast<size_t>(kKnnSmemBudget);
+        int warps = 4;
+        if (!global_heap)
+            while (warps > 1 && warps * (per_warp_heap + per_warp_fixed) > static_cast<size_t>(kKnnSmemBudget))
+                warps >>= 1;
+        const size_t smem = warps * (per_warp_fixed + (global_heap ? 0 : per_warp_heap));
+        const u64 tiles = (q.m + 31) / 32;
+        int per_sm = std::max(1, static_cast<int>(220 * 1024 / std::max<size_t>(smem, 1)));
+        per_sm = std::min(per_sm, 16);
+        const int blocks = static_cast<int>(std::max<u64>(
+            1, std::min<u64>((tiles + warps - 1) / warps, static_cast<u64>(ctx->sm_count) * per_sm)));
+        stage_begin(ctx, "knn");
+        if (q.m) {
+            if (global_heap) {
+                gd = dalloc_t<double>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
+                gi = dalloc_t<u32>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
+                LO_CUDA(cudaFuncSetAttribute(knn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem)));
+                knn_kernel<true><<<blocks, 32 * warps, smem, ctx->stream>>>(
+                    t->tn, c->x, c->y, c->z, q, kh, kh, out->idx, out->dist, gd, gi);
+            } else {
+                LO_CUDA(cudaFuncSetAttribute(knn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem)));
+                knn_kernel<false><<<blocks, 32 * warps, smem, ctx->stream>>>(
+                    t->tn, c->x, c->y, c->z, q, kh, kh, out->idx, out->dist, nullptr, nullptr);
+            }
+            LO_CHECK_LAUNCH();
+        }
+        stage_end(ctx);
+        if (fingerprint) {
+            out->fps = dalloc_t<u64>(ctx, q.m);
+            if (q.m) {
+                knn_digest<<<std::max(1, ceil_div(q.m, 256)), 256, 0, ctx->stream>>>(
+                    out->idx, out->dist, q.m, kh, out->fps);
+                LO_CHECK_LAUNCH();
+            }
+        }
+        LO_CUDA(cudaEventRecord(e1, ctx->stream));
+        sync(ctx);
+        LO_CUDA(cudaEventElapsedTime(&out->ms, e0, e1));
+    } catch (...) {
+        dfree(ctx, out->idx);
+        dfree(ctx, out->dist);
+        dfree(ctx, out->fps);
+        dfree(ctx, gd);
+        dfree(ctx, gi);
+        delete out;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        throw;
+    }
+    dfree(ctx, gd);
+    dfree(ctx, gi);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return out;
+}
+
+}  // namespace lo
+
+using namespace lo;
+
+extern "C" {
+
+int lo_knn(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32_t k,
+           const uint32_t* centres_host, uint64_t m, int fingerprint, lo_knn_result** out) {
+    return api([&] {
+        require(k >= 1, LO_INVALID_ARGUMENT, "knn: k must be >= 1");
+        require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
+        const u64 rows = centres_host ? m : coded->n;
+        u32* cidx = upload_centres(ctx, centres_host, m, coded->n);
+        Queries q{coded->x, coded->y, coded->z, cidx, rows};
+        try {
+            *out = knn_search(ctx, tree, coded, k, q, fingerprint != 0);
+        } catch (...) {
+            dfree(ctx, cidx);
+            throw;
+        }
+        dfree(ctx, cidx);
+    });
+}
+
+int lo_knn_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32_t k,
+                  const double* queries_host, uint64_t m, lo_knn_result** out) {
+    return api([&] {
+        require(k >= 1, LO_INVALID_ARGUMENT, "knn: k must be >= 1");
+        double *x = nullptr, *y = nullptr, *z = nullptr;
+        if (m) upload_points(ctx, queries_host, m, &x, &y, &z);
+        Queries q{x, y, z, nullptr, m};
+        try {
+            *out = knn_search(ctx, tree, coded, k, q, true);
+        } catch (...) {
+            dfree(ctx, x), dfree(ctx, y), dfree(ctx, z);
+            throw;
+        }
+        dfree(ctx, x), dfree(ctx, y), dfree(ctx, z);
+    });
+}
+
+int lo_knn_info_get(const lo_knn_result* res, uint64_t* rows, uint32_t* k_eff, double* device_ms) {
+    return api([&] {
+        if (rows) *rows = res->rows;
+        if (k_eff) *k_eff = res->keff;
+        if (device_ms) *device_ms = res->ms;
+    });
+}
+
+int lo_knn_download(lo_context* ctx, const lo_knn_result* res, uint32_t* idx_host, double* dist_host,
+                    uint64_t* fingerprints_host) {
+    return api([&] {
+        const u64 e = res->rows * res->keff;
+        if (idx_host && e)
+            LO_CUDA(cudaMemcpyAsync(idx_host, res->idx, 4 * e, cudaMemcpyDeviceToHost, ctx->stream));
+        if (dist_host && e)
+            LO_CUDA(cudaMemcpyAsync(dist_host, res->dist, 8 * e, cudaMemcpyDeviceToHost, ctx->stream));
+        if (fingerprints_host && res->rows) {
+            require(res->fps != nullptr, LO_INVALID_ARGUMENT, "fingerprints were not computed");
+            LO_CUDA(cudaMemcpyAsync(fingerprints_host, res->fps, 8 * res->rows,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        sync(ctx);
+    });
+}
+
+int lo_knn_destroy(lo_knn_result* res) {
+    return api([&] {
+        if (!res) return;
+        lo_context* ctx = res->ctx;
+        dfree(ctx, res->idx);
+        dfree(ctx, res->dist);
+        dfree(ctx, res->fps);
+        delete res;
+    });
+}
+
+int lo_locality_log2(lo_context* ctx, const lo_knn_result* res, const lo_coded* coded,
+                     const uint32_t* centres_host, int use_perm, uint64_t* bins33_host) {
+    return api([&] {
+        u32* cidx = upload_centres(ctx, centres_host, centres_host ? res->rows : 0, coded->n);
+        unsigned long long* bins = dalloc_t<unsigned long long>(ctx, 33);
+        LO_CUDA(cudaMemsetAsync(bins, 0, 33 * 8, ctx->stream));
+        const u64 e = res->rows * res->keff;
+        if (e)
+            locality_kernel<<<std::max(1, std::min(ceil_div(e, 256), ctx->sm_count * 8)), 256, 0,
+                              ctx->stream>>>(res->idx, res->rows, res->keff, cidx,
+                                             use_perm ? coded->perm : nullptr, bins);
+        LO_CHECK_LAUNCH();
+        LO_CUDA(cudaMemcpyAsync(bins33_host, bins, 33 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        dfree(ctx, bins);
+        dfree(ctx, cidx);
+        sync(ctx);
+    });
+}
+
+}  // extern "C"

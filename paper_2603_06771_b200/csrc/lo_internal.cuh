@@ -1,0 +1,249 @@
+// lo_internal.cuh -- shared types and device helpers of the B200 path (sm_100a only).
+//
+// Everything FP64 here is compiled with -fmad=false so the device evaluates exactly the
+// reference's expression trees: ((dx*dx + dy*dy) + dz*dz) with
+// no DFMA contraction.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/linoct_b200.h"
+
+namespace lo {
+
+using u8 = std::uint8_t;
+using u32 = std::uint32_t;
+using u64 = std::uint64_t;
+using i32 = std::int32_t;
+using i64 = std::int64_t;
+
+constexpr int kMaxLevel = 21;
+
+// ---- errors ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+    int status;
+    Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+#define LO_CUDA(call)                                                          \
+    do {                                                                       \
+        cudaError_t e_ = (call);                                               \
+        if (e_ != cudaSuccess) ::lo::throw_cuda(e_, #call, __FILE__, __LINE__); \
+    } while (0)
+#define LO_CHECK_LAUNCH() LO_CUDA(cudaGetLastError())
+
+inline void require(bool ok, int status, const std::string& msg) {
+    if (!ok) throw Error(status, msg);
+}
+
+// ---- curve tables (CurveStepper, sfc.hpp:143-164) -----------------------------------------
+// enc[s*8 + g] = (code digit c) | (next state << 3) for octant digit g = x<<2|y<<1|z;
+// dec[s*8 + c] = (octant digit g) | (next state << 3).  Morton has 1 state, Hilbert 24.
+struct CurveTables {
+    u8 enc[32 * 8];
+    u8 dec[32 * 8];
+    int states;
+};
+const CurveTables& curve_tables(int curve);  // host-derived once from the codec (tables.cpp)
+
+// ---- device-side handles ----------------------------------------------------------------
+// Traversal node: non-empty octree nodes in a children-contiguous layout (root = 0).  The
+// box is the exact (tight) min/max of the node's points: any box that contains a node's
+// points gives the reference's result sets under exact non-FMA arithmetic.
+struct __align__(16) TNode {
+    double lo[3];
+    double hi[3];
+    u32 begin, end;    // sorted-cloud index range [begin, end)
+    u32 child0;        // first child tnode (children contiguous, code order)
+    u32 nchild;        // 0 for a leaf
+};
+static_assert(sizeof(TNode) == 64, "TNode must be 64 bytes");
+
+}  // namespace lo
+
+struct lo_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool timing = false;
+    int sm_count = 148;
+    struct Stage {
+        std::string name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Stage> stages;          // pending stage events (resolved on query)
+    std::vector<std::pair<std::string, float>> stage_ms;
+    void* pinned_scratch = nullptr;     // small pinned buffer for scalar D2H
+};
+
+struct lo_coded {
+    lo_context* ctx = nullptr;
+    lo::u64 n = 0;
+    int curve = 0, level = lo::kMaxLevel;
+    double disc_box[6] = {};
+    double cloud_box[6] = {};
+    double scale[3] = {};
+    double *x = nullptr, *y = nullptr, *z = nullptr;  // sorted SoA coordinates
+    lo::u64* codes = nullptr;                         // sorted codes
+    lo::u32* perm = nullptr;                          // perm[new] = old
+};
+
+struct lo_octree {
+    lo_context* ctx = nullptr;
+    const lo_coded* coded = nullptr;
+    lo::u64 points = 0, leaves = 0, internal = 0, tnodes = 0;
+    lo::i32 root = 0;
+    lo::u32 n_max = 0;
+    int level = lo::kMaxLevel, curve = 0;
+    double disc_box[6] = {};
+    lo::u64* bounds = nullptr;          // [leaves+1]
+    lo::u32* offsets = nullptr;         // [leaves+1]
+    lo_internal_node* nodes = nullptr;  // [internal]
+    lo::TNode* tn = nullptr;            // [tnodes]
+    int max_depth = 0;
+};
+
+struct lo_csr {
+    lo_context* ctx = nullptr;
+    lo::u64 rows = 0, total = 0;
+    double mean = 0.0;
+    float ms = 0.f;
+    lo::u64* offsets = nullptr;   // [rows+1]
+    lo::u32* indices = nullptr;   // [total]
+    lo::u32* counts = nullptr;    // [rows]
+    lo::u64* fps = nullptr;       // [rows] or null
+};
+
+struct lo_knn_result {
+    lo_context* ctx = nullptr;
+    lo::u64 rows = 0;
+    lo::u32 k = 0, keff = 0;
+    float ms = 0.f;
+    lo::u32* idx = nullptr;      // [rows*keff]
+    double* dist = nullptr;      // [rows*keff]
+    lo::u64* fps = nullptr;      // [rows] or null
+};
+
+namespace lo {
+
+// ---- memory + timing helpers (context.cu) ------------------------------------------------
+void* dalloc(lo_context* ctx, size_t bytes);
+void dfree(lo_context* ctx, void* p);
+template <class T>
+T* dalloc_t(lo_context* ctx, size_t count) {
+    return static_cast<T*>(dalloc(ctx, count * sizeof(T) + (count == 0)));
+}
+void stage_begin(lo_context* ctx, const char* name);
+void stage_end(lo_context* ctx);
+void sync(lo_context* ctx);
+template <class T>
+T read_scalar(lo_context* ctx, const T* dev) {
+    LO_CUDA(cudaMemcpyAsync(ctx->pinned_scratch, dev, sizeof(T), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    sync(ctx);
+    T v;
+    std::memcpy(&v, ctx->pinned_scratch, sizeof(T));
+    return v;
+}
+
+// scan.cu: exclusive scan, out has n+1 entries (out[n] = total)
+void exclusive_scan_u32_to_u64(lo_context* ctx, const u32* in, u64* out, u64 n);
+void exclusive_scan_u32(lo_context* ctx, const u32* in, u32* out, u64 n);
+
+// ---- device helpers ---------------------------------------------------------------------
+__host__ __device__ inline u64 spread3(u64 v) {
+    v &= 0x1fffffULL;
+    v = (v | v << 32) & 0x001f00000000ffffULL;
+    v = (v | v << 16) & 0x001f0000ff0000ffULL;
+    v = (v | v << 8) & 0x100f00f00f00f00fULL;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
+    v = (v | v << 2) & 0x1249249249249249ULL;
+    return v;
+}
+__host__ __device__ inline u32 compact3(u64 v) {
+    v &= 0x1249249249249249ULL;
+    v = (v ^ (v >> 2)) & 0x10c30c30c30c30c3ULL;
+    v = (v ^ (v >> 4)) & 0x100f00f00f00f00fULL;
+    v = (v ^ (v >> 8)) & 0x001f0000ff0000ffULL;
+    v = (v ^ (v >> 16)) & 0x001f00000000ffffULL;
+    v = (v ^ (v >> 32)) & 0x1fffffULL;
+    return static_cast<u32>(v);
+}
+
+// Order-preserving integer image of a double (exact min/max via integer atomics).
+__host__ __device__ inline u64 dbl_order_key(double v) {
+#ifdef __CUDA_ARCH__
+    const u64 u = static_cast<u64>(__double_as_longlong(v));
+#else
+    u64 u;
+    std::memcpy(&u, &v, 8);
+#endif
+    return (u & 0x8000000000000000ULL) ? ~u : (u | 0x8000000000000000ULL);
+}
+__host__ __device__ inline double dbl_from_order_key(u64 k) {
+    const u64 u = (k & 0x8000000000000000ULL) ? (k & 0x7fffffffffffffffULL) : ~k;
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(static_cast<long long>(u));
+#else
+    double v;
+    std::memcpy(&v, &u, 8);
+    return v;
+#endif
+}
+
+// FNV-1a-64 of a u32 index widened to u64 (search.cpp:263-271): the 4 zero high bytes only
+// multiply, so they fold into one multiplication by prime^5 after the 4th byte.
+__device__ __forceinline__ u64 fnv_u32(u64 h, u32 v) {
+    constexpr u64 P = 0x100000001b3ULL;
+    constexpr u64 P5 = P * P * P * P * P;
+    h ^= v & 0xffu;
+    h *= P;
+    h ^= (v >> 8) & 0xffu;
+    h *= P;
+    h ^= (v >> 16) & 0xffu;
+    h *= P;
+    h ^= v >> 24;
+    h *= P5;
+    return h;
+}
+__device__ __forceinline__ u64 fnv_u64(u64 h, u64 v) {
+    constexpr u64 P = 0x100000001b3ULL;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        h ^= (v >> (8 * i)) & 0xffu;
+        h *= P;
+    }
+    return h;
+}
+constexpr u64 kFnvOffset = 0xcbf29ce484222325ULL;
+
+void set_last_error(const char* msg);
+
+// Runs an API body, mapping exceptions to status codes (no exception crosses the C ABI).
+template <class F>
+int api(F&& f) {
+    try {
+        f();
+        return LO_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return LO_OUT_OF_MEMORY;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return LO_LOGIC_ERROR;
+    }
+}
+
+inline int ceil_div(u64 a, u64 b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace lo

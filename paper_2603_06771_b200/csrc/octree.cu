@@ -1,0 +1,526 @@
+// octree.cu -- K5 parallel linear-octree build over the sorted codes.
+//
+// Replaces build_leaves + link_internal (linear_octree.cpp:23-137) with a scan-based build
+// that produces byte-identical LeafArray and preorder InternalNode tables:
+//
+//  * A depth-d block is internal iff it holds more than n_max points and d < level
+//    (linear_octree.cpp:44-49); all its ancestors then are too.
+//  * Point i opens the internal node at depth d iff it is the block's first point,
+//    cpl(code[i-1], code[i]) < d, and the block overflows, cpl(code[i], code[i+n_max]) >= d,
+//    where cpl = common octal-prefix length.  Preorder (linear_octree.cpp:113-137) equals
+//    the order (first point, depth), so an exclusive scan of per-point counts numbers the
+//    internal nodes exactly as the reference's recursion does.
+//  * Leaves are the non-internal children of internal nodes (empty ones included).  The
+//    leaves before node k's block are 7*(k - depth) + (sum of the prefix's top octal
+//    digits), so each node numbers its own leaf children without a global pass.
+//
+// The traversal side gets a second, children-contiguous table of non-empty nodes (TNode)
+// with tight boxes built bottom-up (Karras-style arrival counters).
+#include <algorithm>
+#include <cmath>
+
+#include "lo_internal.cuh"
+
+namespace lo {
+
+__device__ __forceinline__ int cpl_of(u64 a, u64 b, int level) {
+    if (a == b) return level;
+    return (__clzll(static_cast<long long>(a ^ b)) - (64 - 3 * level)) / 3;
+}
+
+__device__ __forceinline__ u32 lower_bound_dev(const u64* __restrict__ codes, u32 lo, u32 hi,
+                                               u64 key) {
+    while (lo < hi) {
+        const u32 mid = lo + ((hi - lo) >> 1);
+        if (codes[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int first_open_depth(const u64* __restrict__ codes, u64 i, int level) {
+    return i == 0 ? 0 : cpl_of(codes[i - 1], codes[i], level) + 1;
+}
+
+// number of internal nodes whose first point is i
+__global__ void open_count(const u64* __restrict__ codes, u64 n, u32 n_max, int level,
+                           u32* __restrict__ cnt) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        u32 c = 0;
+        if (i + n_max < n && level > 0) {
+            const int lo = first_open_depth(codes, i, level);
+            const int hi = min(level - 1, cpl_of(codes[i], codes[i + n_max], level));
+            c = hi >= lo ? static_cast<u32>(hi - lo + 1) : 0u;
+        }
+        cnt[i] = c;
+    }
+}
+
+__global__ void open_emit(const u64* __restrict__ codes, u64 n, const u32* __restrict__ cnt,
+                          const u32* __restrict__ S, int level, u32* __restrict__ npoint,
+                          u8* __restrict__ ndepth) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u32 c = cnt[i];
+        if (c == 0) continue;
+        const int lo = first_open_depth(codes, i, level);
+        const u32 base = S[i];
+        for (u32 t = 0; t < c; ++t) {
+            npoint[base + t] = static_cast<u32>(i);
+            ndepth[base + t] = static_cast<u8>(lo + t);
+        }
+    }
+}
+
+// One thread per internal node: range, children, child mask, leaf children.
+__global__ void link_nodes(const u64* __restrict__ codes, u32 n, u32 n_max, int level,
+                           const u32* __restrict__ S, const u32* __restrict__ npoint,
+                           const u8* __restrict__ ndepth, u32 internal,
+                           lo_internal_node* __restrict__ nodes, u64* __restrict__ bounds,
+                           u32* __restrict__ offsets, u32* __restrict__ nchild) {
+    for (u64 k = blockIdx.x * (u64)blockDim.x + threadIdx.x; k < internal;
+         k += (u64)gridDim.x * blockDim.x) {
+        const u32 i = npoint[k];
+        const int d = ndepth[k];
+        const int shift = 3 * (level - d);
+        const u64 span = 1ull << shift;
+        const u64 prefix = d == 0 ? 0ull : (codes[i] >> shift) << shift;
+        const u32 end = lower_bound_dev(codes, i, n, prefix + span);
+        const u64 sub = span >> 3;
+        u64 leaf = 7ull * (k - static_cast<u64>(d));
+        for (int t = 1; t <= d; ++t) leaf += (prefix >> (3 * (level - t))) & 7u;
+        u32 cb[9];
+        cb[0] = i;
+        cb[8] = end;
+        for (int c = 1; c < 8; ++c) cb[c] = lower_bound_dev(codes, cb[c - 1], end, prefix + c * sub);
+        lo_internal_node nd;
+        nd.prefix = prefix;
+        nd.begin = i;
+        nd.end = end;
+        nd.depth = static_cast<u8>(d);
+        u8 mask = 0;
+        for (int c = 0; c < 8; ++c) {
+            const u32 count = cb[c + 1] - cb[c];
+            if (count > n_max && d + 1 < level) {
+                const u32 j = S[cb[c]] + static_cast<u32>(d + 1 - first_open_depth(codes, cb[c], level));
+                nd.children[c] = static_cast<i32>(j);
+                leaf += 1 + 7ull * (S[cb[c + 1]] - j);
+            } else {
+                nd.children[c] = ~static_cast<i32>(leaf);
+                bounds[leaf] = prefix + c * sub;
+                offsets[leaf] = cb[c];
+                ++leaf;
+            }
+            if (count) mask |= static_cast<u8>(1u << c);
+        }
+        nd.child_mask = mask;
+        for (int b = 0; b < 6; ++b) nd.pad_[b] = 0;
+        nodes[k] = nd;
+        nchild[k] = __popc(mask);
+    }
+}
+
+__global__ void leaves_tail(u64* bounds, u32* offsets, u64 leaves, u64 full, u32 n) {
+    bounds[leaves] = full;
+    offsets[leaves] = n;
+    if (leaves == 1) {  // single-leaf tree: root leaf covers everything
+        bounds[0] = 0;
+        offsets[0] = 0;
+    }
+}
+
+// TNode table: root = 0; the non-empty children of internal node k sit at
+// 1 + tbase[k] + rank, in code order.
+__global__ void emit_tnodes(const lo_internal_node* __restrict__ nodes, u32 internal,
+                            const u32* __restrict__ tbase, const u32* __restrict__ nchild,
+                            const u32* __restrict__ offsets, TNode* __restrict__ tn,
+                            u32* __restrict__ parent, u32* __restrict__ tid_of) {
+    for (u64 k = blockIdx.x * (u64)blockDim.x + threadIdx.x; k < internal;
+         k += (u64)gridDim.x * blockDim.x) {
+        const lo_internal_node nd = nodes[k];
+        u32 t = 1 + tbase[k];
+        if (k == 0) {
+            tn[0].begin = nd.begin;
+            tn[0].end = nd.end;
+            tn[0].child0 = 1 + tbase[0];
+            tn[0].nchild = nchild[0];
+            parent[0] = ~0u;
+            tid_of[0] = 0;
+        }
+        for (int c = 0; c < 8; ++c) {
+            if (!((nd.child_mask >> c) & 1)) continue;
+            const i32 ch = nd.children[c];
+            TNode& o = tn[t];
+            if (ch >= 0) {
+                const lo_internal_node& cn = nodes[ch];
+                o.begin = cn.begin;
+                o.end = cn.end;
+                o.child0 = 1 + tbase[ch];
+                o.nchild = nchild[ch];
+                tid_of[ch] = t;
+            } else {
+                o.begin = offsets[~ch];
+                o.end = offsets[~ch + 1];
+                o.child0 = 0;
+                o.nchild = 0;
+            }
+            parent[t] = static_cast<u32>(k);
+            ++t;
+        }
+    }
+}
+
+__global__ void single_leaf_tnode(TNode* tn, u32 n, u32* parent) {
+    tn[0].begin = 0;
+    tn[0].end = n;
+    tn[0].child0 = 0;
+    tn[0].nchild = 0;
+    parent[0] = ~0u;
+}
+
+// Leaf boxes from their points, then bottom-up unions: the last child to arrive at a parent
+// (arrival counter) computes the parent's box and continues upward.
+__global__ void tnode_boxes(TNode* tn, u64 tnodes, const double* __restrict__ x,
+                            const double* __restrict__ y, const double* __restrict__ z,
+                            const u32* __restrict__ parent, const u32* __restrict__ tid_of,
+                            u32* __restrict__ arrivals) {
+    for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < tnodes;
+         t += (u64)gridDim.x * blockDim.x) {
+        const u32 nch = tn[t].nchild;
+        if (nch != 0) continue;
+        const u32 b = tn[t].begin, e = tn[t].end;
+        double lo[3] = {x[b], y[b], z[b]}, hi[3] = {x[b], y[b], z[b]};
+        for (u32 i = b + 1; i < e; ++i) {
+            const double v[3] = {x[i], y[i], z[i]};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = fmin(lo[a], v[a]);
+                hi[a] = fmax(hi[a], v[a]);
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            tn[t].lo[a] = lo[a];
+            tn[t].hi[a] = hi[a];
+        }
+        u32 cur = parent[t];
+        while (cur != ~0u) {
+            __threadfence();
+            if (atomicAdd(&arrivals[cur], 1u) + 1 != tn[tid_of[cur]].nchild) break;
+            __threadfence();
+            const u32 pt = tid_of[cur];
+            const u32 c0 = __ldcg(&tn[pt].child0);
+            const u32 nc = __ldcg(&tn[pt].nchild);
+            double plo[3], phi[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                plo[a] = __ldcg(&tn[c0].lo[a]);
+                phi[a] = __ldcg(&tn[c0].hi[a]);
+            }
+            for (u32 c = 1; c < nc; ++c) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    plo[a] = fmin(plo[a], __ldcg(&tn[c0 + c].lo[a]));
+                    phi[a] = fmax(phi[a], __ldcg(&tn[c0 + c].hi[a]));
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                __stcg(&tn[pt].lo[a], plo[a]);
+                __stcg(&tn[pt].hi[a], phi[a]);
+            }
+            cur = parent[pt];
+        }
+    }
+}
+
+// node_bounds (linear_octree.cpp:139-147): padded octant box of a NodeRef.
+struct BoundsParams {
+    double box[6];
+    int level;
+    u8 dec[32 * 8];
+};
+
+__device__ __forceinline__ double pad_down(double v) { return dbl_from_order_key(dbl_order_key(v) - 2); }
+__device__ __forceinline__ double pad_up(double v) { return dbl_from_order_key(dbl_order_key(v) + 2); }
+
+__global__ void node_bounds_kernel(const i32* __restrict__ refs, u64 count,
+                                   const lo_internal_node* __restrict__ nodes,
+                                   const u64* __restrict__ bounds, BoundsParams p,
+                                   double* __restrict__ out) {
+    for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < count;
+         r += (u64)gridDim.x * blockDim.x) {
+        const i32 ref = refs[r];
+        u64 prefix;
+        int depth;
+        if (ref < 0) {
+            const u32 id = static_cast<u32>(~ref);
+            prefix = bounds[id];
+            const u64 span = bounds[id + 1] - bounds[id];
+            depth = p.level - (__ffsll(static_cast<long long>(span)) - 1) / 3;
+        } else {
+            prefix = nodes[ref].prefix;
+            depth = nodes[ref].depth;
+        }
+        double* o = out + 6 * r;
+        if (depth == 0) {
+            for (int a = 0; a < 6; ++a) o[a] = p.box[a];
+            continue;
+        }
+        const u64 top = prefix >> (3 * (p.level - depth));
+        u32 h[3] = {0, 0, 0}, s = 0;
+        for (int d = depth - 1; d >= 0; --d) {
+            const u32 e = p.dec[s * 8 + ((top >> (3 * d)) & 7u)];
+            h[0] = h[0] << 1 | ((e >> 2) & 1u);
+            h[1] = h[1] << 1 | ((e >> 1) & 1u);
+            h[2] = h[2] << 1 | (e & 1u);
+            s = e >> 3;
+        }
+        const double inv = ldexp(1.0, -depth);
+        for (int a = 0; a < 3; ++a) {
+            const double side = (p.box[3 + a] - p.box[a]) * inv;
+            const double lo = p.box[a] + static_cast<double>(h[a]) * side;
+            const double hi = lo + side;
+            o[a] = pad_down(lo);
+            o[3 + a] = pad_up(hi);
+        }
+    }
+}
+
+__global__ void check_sorted(const u64* __restrict__ codes, u64 n, u64 full, u32* __restrict__ flags) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        if (i > 0 && codes[i - 1] > codes[i]) atomicOr(flags, 1u);
+        if (codes[i] >= full) atomicOr(flags, 2u);
+    }
+}
+
+static int grid1(lo_context* ctx, u64 n, int threads = 256) {
+    const u64 want = (n + threads - 1) / threads;
+    return static_cast<int>(std::max<u64>(1, std::min<u64>(want, static_cast<u64>(ctx->sm_count) * 16)));
+}
+
+struct LeafBuild {
+    u64 internal = 0, leaves = 0;
+    u64* bounds = nullptr;
+    u32* offsets = nullptr;
+    lo_internal_node* nodes = nullptr;
+    u32* nchild = nullptr;
+    int max_depth = 0;
+};
+
+// Internal-node table + LeafArray for sorted device codes.
+static LeafBuild build_tables(lo_context* ctx, const u64* codes, u64 n, u32 n_max, int level) {
+    LeafBuild r;
+    u32* cnt = dalloc_t<u32>(ctx, n);
+    u32* S = dalloc_t<u32>(ctx, n + 1);
+    open_count<<<grid1(ctx, n), 256, 0, ctx->stream>>>(codes, n, n_max, level, cnt);
+    LO_CHECK_LAUNCH();
+    exclusive_scan_u32(ctx, cnt, S, n);
+    const u32 I = read_scalar(ctx, S + n);
+    r.internal = I;
+    r.leaves = 7ull * I + 1;
+    r.bounds = dalloc_t<u64>(ctx, r.leaves + 1);
+    r.offsets = dalloc_t<u32>(ctx, r.leaves + 1);
+    r.nodes = dalloc_t<lo_internal_node>(ctx, I);
+    r.nchild = dalloc_t<u32>(ctx, I + 1);
+    if (I > 0) {
+        u32* npoint = dalloc_t<u32>(ctx, I);
+        u8* ndepth = dalloc_t<u8>(ctx, I);
+        open_emit<<<grid1(ctx, n), 256, 0, ctx->stream>>>(codes, n, cnt, S, level, npoint, ndepth);
+        LO_CHECK_LAUNCH();
+        link_nodes<<<grid1(ctx, I, 128), 128, 0, ctx->stream>>>(
+            codes, static_cast<u32>(n), n_max, level, S, npoint, ndepth, I, r.nodes, r.bounds,
+            r.offsets, r.nchild);
+        LO_CHECK_LAUNCH();
+        dfree(ctx, npoint);
+        dfree(ctx, ndepth);
+    }
+    const u64 full = 1ull << (3 * level);
+    leaves_tail<<<1, 1, 0, ctx->stream>>>(r.bounds, r.offsets, r.leaves, full, static_cast<u32>(n));
+    LO_CHECK_LAUNCH();
+    dfree(ctx, cnt);
+    dfree(ctx, S);
+    return r;
+}
+
+static void validate_codes(lo_context* ctx, const u64* codes, u64 n, int level) {
+    u32* flags = dalloc_t<u32>(ctx, 1);
+    LO_CUDA(cudaMemsetAsync(flags, 0, 4, ctx->stream));
+    check_sorted<<<grid1(ctx, n), 256, 0, ctx->stream>>>(codes, n, 1ull << (3 * level), flags);
+    LO_CHECK_LAUNCH();
+    const u32 f = read_scalar(ctx, flags);
+    dfree(ctx, flags);
+    require(!(f & 1u), LO_INVALID_ARGUMENT, "build_leaves: codes are not sorted");
+    require(!(f & 2u), LO_INVALID_ARGUMENT, "build_leaves: code exceeds 8^level");
+}
+
+static lo_octree* octree_build(lo_context* ctx, const lo_coded* coded, u32 n_max) {
+    require(coded != nullptr, LO_INVALID_ARGUMENT, "null coded cloud");
+    require(n_max >= 1, LO_INVALID_ARGUMENT, "build_leaves: n_max must be >= 1");
+    const u64 n = coded->n;
+    stage_begin(ctx, "build");
+    LeafBuild lb = build_tables(ctx, coded->codes, n, n_max, coded->level);
+    auto* t = new lo_octree;
+    t->ctx = ctx;
+    t->coded = coded;
+    t->points = n;
+    t->leaves = lb.leaves;
+    t->internal = lb.internal;
+    t->root = lb.internal > 0 ? 0 : ~0;
+    t->n_max = n_max;
+    t->level = coded->level;
+    t->curve = coded->curve;
+    std::memcpy(t->disc_box, coded->disc_box, sizeof t->disc_box);
+    t->bounds = lb.bounds;
+    t->offsets = lb.offsets;
+    t->nodes = lb.nodes;
+    const u32 I = static_cast<u32>(lb.internal);
+    // traversal table
+    u32* tbase = dalloc_t<u32>(ctx, I + 1);
+    u64 T = 1;
+    if (I > 0) {
+        exclusive_scan_u32(ctx, lb.nchild, tbase, I);
+        T = 1 + read_scalar(ctx, tbase + I);
+    }
+    t->tnodes = T;
+    t->tn = dalloc_t<TNode>(ctx, T);
+    u32* parent = dalloc_t<u32>(ctx, T);
+    u32* tid_of = dalloc_t<u32>(ctx, I + 1);
+    u32* arrivals = dalloc_t<u32>(ctx, I + 1);
+    LO_CUDA(cudaMemsetAsync(arrivals, 0, 4ull * (I + 1), ctx->stream));
+    if (I > 0) {
+        emit_tnodes<<<grid1(ctx, I, 128), 128, 0, ctx->stream>>>(lb.nodes, I, tbase, lb.nchild,
+                                                                 lb.offsets, t->tn, parent, tid_of);
+    } else {
+        single_leaf_tnode<<<1, 1, 0, ctx->stream>>>(t->tn, static_cast<u32>(n), parent);
+    }
+    LO_CHECK_LAUNCH();
+    tnode_boxes<<<grid1(ctx, T, 128), 128, 0, ctx->stream>>>(t->tn, T, coded->x, coded->y,
+                                                              coded->z, parent, tid_of, arrivals);
+    LO_CHECK_LAUNCH();
+    stage_end(ctx);
+    dfree(ctx, tbase);
+    dfree(ctx, parent);
+    dfree(ctx, tid_of);
+    dfree(ctx, arrivals);
+    dfree(ctx, lb.nchild);
+    sync(ctx);
+    return t;
+}
+
+}  // namespace lo
+
+using namespace lo;
+
+extern "C" {
+
+int lo_build_leaves(lo_context* ctx, const uint64_t* codes_host, uint64_t n, uint32_t n_max,
+                    int level, uint64_t* leaves, uint64_t* boundaries_host, uint32_t* offsets_host,
+                    uint64_t cap) {
+    return api([&] {
+        require(n_max >= 1, LO_INVALID_ARGUMENT, "build_leaves: n_max must be >= 1");
+        require(n > 0, LO_INVALID_ARGUMENT, "build_leaves: empty code array");
+        require(level >= 0 && level <= kMaxLevel, LO_INVALID_ARGUMENT, "level out of range");
+        require(n <= 0xffffffffull, LO_INVALID_ARGUMENT, "build_leaves: too many codes");
+        u64* codes = dalloc_t<u64>(ctx, n);
+        LO_CUDA(cudaMemcpyAsync(codes, codes_host, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+        try {
+            validate_codes(ctx, codes, n, level);
+        } catch (...) {
+            dfree(ctx, codes);
+            throw;
+        }
+        LeafBuild lb = build_tables(ctx, codes, n, n_max, level);
+        *leaves = lb.leaves;
+        if (boundaries_host && cap >= lb.leaves + 1) {
+            LO_CUDA(cudaMemcpyAsync(boundaries_host, lb.bounds, 8 * (lb.leaves + 1),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+            LO_CUDA(cudaMemcpyAsync(offsets_host, lb.offsets, 4 * (lb.leaves + 1),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        dfree(ctx, codes);
+        dfree(ctx, lb.bounds);
+        dfree(ctx, lb.offsets);
+        dfree(ctx, lb.nodes);
+        dfree(ctx, lb.nchild);
+        sync(ctx);
+        require(boundaries_host == nullptr || cap >= lb.leaves + 1, LO_INVALID_ARGUMENT,
+                "build_leaves: output capacity too small");
+    });
+}
+
+int lo_octree_build(lo_context* ctx, const lo_coded* coded, uint32_t n_max, lo_octree** out) {
+    return api([&] { *out = octree_build(ctx, coded, n_max); });
+}
+
+int lo_octree_info_get(const lo_octree* t, lo_octree_info* out) {
+    return api([&] {
+        require(t != nullptr, LO_INVALID_ARGUMENT, "null octree");
+        out->leaves = t->leaves;
+        out->internal = t->internal;
+        out->root = t->root;
+        out->n_max = t->n_max;
+        out->level = t->level;
+        out->curve = t->curve;
+        out->points = t->points;
+        out->tnodes = t->tnodes;
+    });
+}
+
+int lo_octree_download(lo_context* ctx, const lo_octree* t, uint64_t* boundaries_host,
+                       uint32_t* offsets_host, lo_internal_node* nodes_host) {
+    return api([&] {
+        if (boundaries_host)
+            LO_CUDA(cudaMemcpyAsync(boundaries_host, t->bounds, 8 * (t->leaves + 1),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        if (offsets_host)
+            LO_CUDA(cudaMemcpyAsync(offsets_host, t->offsets, 4 * (t->leaves + 1),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        if (nodes_host && t->internal)
+            LO_CUDA(cudaMemcpyAsync(nodes_host, t->nodes, sizeof(lo_internal_node) * t->internal,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+    });
+}
+
+int lo_octree_node_bounds(lo_context* ctx, const lo_octree* t, const int32_t* refs_host,
+                          uint64_t count, double* boxes_host) {
+    return api([&] {
+        if (count == 0) return;
+        for (u64 r = 0; r < count; ++r) {
+            const i32 ref = refs_host[r];
+            require(ref >= 0 ? static_cast<u64>(ref) < t->internal : static_cast<u64>(~ref) < t->leaves,
+                    LO_INVALID_ARGUMENT, "node_bounds: NodeRef out of range");
+        }
+        i32* refs = dalloc_t<i32>(ctx, count);
+        double* out = dalloc_t<double>(ctx, 6 * count);
+        LO_CUDA(cudaMemcpyAsync(refs, refs_host, 4 * count, cudaMemcpyHostToDevice, ctx->stream));
+        BoundsParams p{};
+        std::memcpy(p.box, t->disc_box, sizeof p.box);
+        p.level = t->level;
+        std::memcpy(p.dec, curve_tables(t->curve).dec, sizeof p.dec);
+        node_bounds_kernel<<<grid1(ctx, count), 256, 0, ctx->stream>>>(refs, count, t->nodes,
+                                                                       t->bounds, p, out);
+        LO_CHECK_LAUNCH();
+        LO_CUDA(cudaMemcpyAsync(boxes_host, out, 48 * count, cudaMemcpyDeviceToHost, ctx->stream));
+        dfree(ctx, refs);
+        dfree(ctx, out);
+        sync(ctx);
+    });
+}
+
+int lo_octree_destroy(lo_octree* t) {
+    return api([&] {
+        if (!t) return;
+        lo_context* ctx = t->ctx;
+        dfree(ctx, t->bounds);
+        dfree(ctx, t->offsets);
+        dfree(ctx, t->nodes);
+        dfree(ctx, t->tn);
+        delete t;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,308 @@
+// radius.cu -- K6 fixed-radius search (count -> u64 scan -> fill) and K8 row digests.
+//
+// Replaces neighbours_lin / neighbours_prune / run_radius_batch (search.cpp:45-156,
+// :261-351).  One warp owns a tile of 32 consecutive queries (SFC-contiguous in Full mode)
+// and walks the octree once for all of them: a node is entered while any lane's query
+// intersects its box; a lane whose query contains the whole node emits the node's index
+// range at once (the Keller-style prune of neighbours_prune) and ignores its descendants;
+// leaf points are staged in shared memory and tested by every intersecting lane with the
+// exact predicate.  DFS visits children in code order, so rows come out ascending like the
+// reference's.
+#include <algorithm>
+#include <cmath>
+
+#include "search_common.cuh"
+
+namespace lo {
+
+constexpr int kRadiusWarps = 4;
+constexpr int kRadiusThreads = 32 * kRadiusWarps;
+
+template <int SHAPE, bool FILL>
+__global__ void __launch_bounds__(kRadiusThreads) radius_kernel(
+    const TNode* __restrict__ tn, const double* __restrict__ px, const double* __restrict__ py,
+    const double* __restrict__ pz, Queries q, double r, double r2, u32* __restrict__ counts,
+    const u64* __restrict__ offsets, u32* __restrict__ out) {
+    __shared__ u32 stack_s[kRadiusWarps][kStackCap];
+    __shared__ double sx[kRadiusWarps][32], sy[kRadiusWarps][32], sz[kRadiusWarps][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    u32* stack = stack_s[w];
+    const u64 ntiles = (q.m + 31) / 32;
+    for (u64 tile = static_cast<u64>(blockIdx.x) * kRadiusWarps + w; tile < ntiles;
+         tile += static_cast<u64>(gridDim.x) * kRadiusWarps) {
+        const u64 qi = tile * 32 + lane;
+        const bool active = qi < q.m;
+        double cx = 0.0, cy = 0.0, cz = 0.0;
+        if (active) load_query(q, qi, cx, cy, cz);
+        u32 count = 0;
+        u32* row = nullptr;
+        if (FILL && active) row = out + offsets[qi];
+        u32 skip_end = 0;
+        int sp = 1;
+        if (lane == 0) stack[0] = 0;
+        __syncwarp();
+        while (sp > 0) {
+            const u32 t = stack[--sp];
+            const NodeView nd = load_node(tn, t);
+            int rel = kDisjoint;
+            if (active && nd.begin >= skip_end) rel = relation<SHAPE>(cx, cy, cz, r, r2, nd);
+            if (rel == kContains) {
+                if (FILL)
+                    for (u32 i = nd.begin; i < nd.end; ++i) row[count + (i - nd.begin)] = i;
+                count += nd.end - nd.begin;
+                skip_end = nd.end;
+            }
+            const unsigned hit = __ballot_sync(~0u, rel == kIntersects);
+            if (!hit) continue;
+            if (nd.nchild == 0) {
+                for (u32 base = nd.begin; base < nd.end; base += 32) {
+                    const u32 j = base + lane;
+                    __syncwarp();
+                    if (j < nd.end) {
+                        sx[w][lane] = px[j];
+                        sy[w][lane] = py[j];
+                        sz[w][lane] = pz[j];
+                    }
+                    __syncwarp();
+                    if (rel == kIntersects) {
+                        const u32 cnt = min(32u, nd.end - base);
+                        for (u32 jj = 0; jj < cnt; ++jj) {
+                            if (contains<SHAPE>(cx, cy, cz, r, r2, sx[w][jj], sy[w][jj], sz[w][jj])) {
+                                if (FILL) row[count] = base + jj;
+                                ++count;
+                            }
+                        }
+                    }
+                }
+            } else {
+                __syncwarp();
+                if (lane < static_cast<int>(nd.nchild)) stack[sp + nd.nchild - 1 - lane] = nd.child0 + lane;
+                sp += nd.nchild;
+                __syncwarp();
+            }
+        }
+        if (!FILL && active) counts[qi] = count;
+        __syncwarp();
+    }
+}
+
+// K8: FNV-1a-64 per row over its indices (search.cpp:345-347).
+__global__ void radius_digest(const u64* __restrict__ offsets, const u32* __restrict__ idx, u64 m,
+                              u64* __restrict__ fps) {
+    for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < m;
+         r += (u64)gridDim.x * blockDim.x) {
+        u64 h = kFnvOffset;
+        const u64 e = offsets[r + 1];
+        for (u64 j = offsets[r]; j < e; ++j) h = fnv_u32(h, idx[j]);
+        fps[r] = h;
+    }
+}
+
+__global__ void counts_from_offsets(const u64* __restrict__ offsets, u64 m, u32* __restrict__ counts) {
+    for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < m;
+         r += (u64)gridDim.x * blockDim.x)
+        counts[r] = static_cast<u32>(offsets[r + 1] - offsets[r]);
+}
+
+template <bool FILL>
+static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const lo_coded* c,
+                          const Queries& q, double r, u32* counts, const u64* offsets, u32* out) {
+    const double r2 = r * r;  // SearchKernel ctor (geometry.hpp:107)
+    const u64 tiles = (q.m + 31) / 32;
+    const int blocks = static_cast<int>(std::max<u64>(1, std::min<u64>((tiles + kRadiusWarps - 1) / kRadiusWarps,
+                                                                      static_cast<u64>(ctx->sm_count) * 64)));
+#define LO_RADIUS_CASE(S)                                                                        \
+    case S:                                                                                      \
+        radius_kernel<S, FILL><<<blocks, kRadiusThreads, 0, ctx->stream>>>(t->tn, c->x, c->y,    \
+                                                                           c->z, q, r, r2,       \
+                                                                           counts, offsets, out); \
+        break;
+    switch (shape) {
+        LO_RADIUS_CASE(LO_SPHERE)
+        LO_RADIUS_CASE(LO_CIRCLE)
+        LO_RADIUS_CASE(LO_CUBE)
+        LO_RADIUS_CASE(LO_SQUARE)
+        default: throw Error(LO_INVALID_ARGUMENT, "unknown kernel shape");
+    }
+#undef LO_RADIUS_CASE
+    LO_CHECK_LAUNCH();
+}
+
+static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded* c, int shape,
+                             double r, const Queries& q, bool fingerprint) {
+    require(t != nullptr && c != nullptr, LO_INVALID_ARGUMENT, "null tree or cloud");
+    require(r > 0.0 && std::isfinite(r), LO_INVALID_ARGUMENT,
+            "kernel radius must be positive and finite");
+    auto* out = new lo_csr;
+    out->ctx = ctx;
+    out->rows = q.m;
+    cudaEvent_t e0, e1;
+    LO_CUDA(cudaEventCreate(&e0));
+    LO_CUDA(cudaEventCreate(&e1));
+    try {
+        LO_CUDA(cudaEventRecord(e0, ctx->stream));
+        out->counts = dalloc_t<u32>(ctx, q.m);
+        out->offsets = dalloc_t<u64>(ctx, q.m + 1);
+        stage_begin(ctx, "radius_count");
+        if (q.m) launch_radius<false>(ctx, shape, t, c, q, r, out->counts, nullptr, nullptr);
+        stage_end(ctx);
+        stage_begin(ctx, "radius_scan");
+        exclusive_scan_u32_to_u64(ctx, out->counts, out->offsets, q.m);
+        stage_end(ctx);
+        out->total = read_scalar(ctx, out->offsets + q.m);
+        out->indices = dalloc_t<u32>(ctx, out->total);
+        stage_begin(ctx, "radius_fill");
+        if (q.m) launch_radius<true>(ctx, shape, t, c, q, r, nullptr, out->offsets, out->indices);
+        stage_end(ctx);
+        if (fingerprint) {
+            out->fps = dalloc_t<u64>(ctx, q.m);
+            stage_begin(ctx, "radius_digest");
+            if (q.m)
+                radius_digest<<<std::max(1, ceil_div(q.m, 256)), 256, 0, ctx->stream>>>(
+                    out->offsets, out->indices, q.m, out->fps);
+            LO_CHECK_LAUNCH();
+            stage_end(ctx);
+        }
+        LO_CUDA(cudaEventRecord(e1, ctx->stream));
+        sync(ctx);
+        LO_CUDA(cudaEventElapsedTime(&out->ms, e0, e1));
+        out->mean = q.m ? static_cast<double>(out->total) / static_cast<double>(q.m) : 0.0;
+    } catch (...) {
+        dfree(ctx, out->counts);
+        dfree(ctx, out->offsets);
+        dfree(ctx, out->indices);
+        dfree(ctx, out->fps);
+        delete out;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        throw;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return out;
+}
+
+// Centre indices from the host (or Full mode when null), validated against the cloud size.
+u32* upload_centres(lo_context* ctx, const u32* centres_host, u64 m, u64 n) {
+    if (!centres_host) return nullptr;
+    for (u64 i = 0; i < m; ++i)
+        require(centres_host[i] < n, LO_INVALID_ARGUMENT, "centre index out of range");
+    u32* d = dalloc_t<u32>(ctx, m);
+    LO_CUDA(cudaMemcpyAsync(d, centres_host, 4 * m, cudaMemcpyHostToDevice, ctx->stream));
+    return d;
+}
+
+// Explicit query points (AoS host) -> SoA device.
+void upload_points(lo_context* ctx, const double* xyz_host, u64 m, double** x, double** y,
+                   double** z) {
+    std::vector<double> sx(m), sy(m), sz(m);
+    for (u64 i = 0; i < m; ++i) {
+        sx[i] = xyz_host[3 * i];
+        sy[i] = xyz_host[3 * i + 1];
+        sz[i] = xyz_host[3 * i + 2];
+        require(std::isfinite(sx[i]) && std::isfinite(sy[i]) && std::isfinite(sz[i]),
+                LO_INVALID_ARGUMENT, "kernel center must be finite");
+    }
+    *x = dalloc_t<double>(ctx, m);
+    *y = dalloc_t<double>(ctx, m);
+    *z = dalloc_t<double>(ctx, m);
+    LO_CUDA(cudaMemcpyAsync(*x, sx.data(), 8 * m, cudaMemcpyHostToDevice, ctx->stream));
+    LO_CUDA(cudaMemcpyAsync(*y, sy.data(), 8 * m, cudaMemcpyHostToDevice, ctx->stream));
+    LO_CUDA(cudaMemcpyAsync(*z, sz.data(), 8 * m, cudaMemcpyHostToDevice, ctx->stream));
+    sync(ctx);
+}
+
+}  // namespace lo
+
+using namespace lo;
+
+extern "C" {
+
+int lo_radius(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int method, int shape,
+              double radius, const uint32_t* centres_host, uint64_t m, int fingerprint,
+              lo_csr** out) {
+    return api([&] {
+        require(method != LO_METHOD_PTR, LO_INVALID_ARGUMENT,
+                "run_radius_batch: ptr method needs a pointer octree");
+        require(method == LO_METHOD_LIN || method == LO_METHOD_PRUNE || method == LO_METHOD_STRUCT,
+                LO_INVALID_ARGUMENT, "unknown radius method");
+        require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
+        const u64 rows = centres_host ? m : coded->n;
+        u32* cidx = upload_centres(ctx, centres_host, m, coded->n);
+        Queries q{coded->x, coded->y, coded->z, cidx, rows};
+        try {
+            *out = radius_search(ctx, tree, coded, shape, radius, q, fingerprint != 0);
+        } catch (...) {
+            dfree(ctx, cidx);
+            throw;
+        }
+        dfree(ctx, cidx);
+    });
+}
+
+int lo_radius_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int shape,
+                     double radius, const double* queries_host, uint64_t m, lo_csr** out) {
+    return api([&] {
+        double *x = nullptr, *y = nullptr, *z = nullptr;
+        if (m) upload_points(ctx, queries_host, m, &x, &y, &z);
+        Queries q{x, y, z, nullptr, m};
+        try {
+            *out = radius_search(ctx, tree, coded, shape, radius, q, true);
+        } catch (...) {
+            dfree(ctx, x), dfree(ctx, y), dfree(ctx, z);
+            throw;
+        }
+        dfree(ctx, x), dfree(ctx, y), dfree(ctx, z);
+    });
+}
+
+int lo_csr_info_get(const lo_csr* csr, lo_csr_info* out) {
+    return api([&] {
+        out->rows = csr->rows;
+        out->total = csr->total;
+        out->mean_count = csr->mean;
+        out->device_ms = csr->ms;
+    });
+}
+
+int lo_csr_download(lo_context* ctx, const lo_csr* csr, uint32_t* counts_host,
+                    uint64_t* fingerprints_host, uint64_t* offsets_host, uint32_t* indices_host) {
+    return api([&] {
+        if (counts_host && csr->rows)
+            LO_CUDA(cudaMemcpyAsync(counts_host, csr->counts, 4 * csr->rows, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+        if (fingerprints_host && csr->rows) {
+            require(csr->fps != nullptr, LO_INVALID_ARGUMENT, "fingerprints were not computed");
+            LO_CUDA(cudaMemcpyAsync(fingerprints_host, csr->fps, 8 * csr->rows,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        if (offsets_host)
+            LO_CUDA(cudaMemcpyAsync(offsets_host, csr->offsets, 8 * (csr->rows + 1),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        if (indices_host && csr->total)
+            LO_CUDA(cudaMemcpyAsync(indices_host, csr->indices, 4 * csr->total,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+    });
+}
+
+int lo_csr_device_ptrs(const lo_csr* csr, const uint64_t** offsets, const uint32_t** indices) {
+    return api([&] {
+        if (offsets) *offsets = csr->offsets;
+        if (indices) *indices = csr->indices;
+    });
+}
+
+int lo_csr_destroy(lo_csr* csr) {
+    return api([&] {
+        if (!csr) return;
+        lo_context* ctx = csr->ctx;
+        dfree(ctx, csr->counts);
+        dfree(ctx, csr->offsets);
+        dfree(ctx, csr->indices);
+        dfree(ctx, csr->fps);
+        delete csr;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,673 @@
+// reorder.cu -- K1 bbox, K2 encode (+ fused digit histograms), K3 onesweep LSD radix sort,
+// K4 SoA gather.  Replaces compute_codes / radix_sort_codes / reorder_cloud
+// (reorder.cpp:9-89) with bit-identical results (keys, stable permutation, coordinates).
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+#include "lo_internal.cuh"
+
+namespace lo {
+
+// ---- K1: exact bbox + finite check (geometry.hpp:64-82) ----------------------------------
+// min/max are taken on the order-preserving integer image, so the reduction is exact and
+// order independent.  bbox[0..2] = min keys, [3..5] = max keys, [6] = first non-finite index.
+__global__ void __launch_bounds__(256) bbox_kernel(const double* __restrict__ xyz, u64 n,
+                                                   u64* __restrict__ out) {
+    u64 mn[3] = {~0ull, ~0ull, ~0ull}, mx[3] = {0, 0, 0};
+    u64 bad = ~0ull;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double v = xyz[3 * i + a];
+            if (!isfinite(v)) bad = min(bad, i);
+            const u64 k = dbl_order_key(v);
+            mn[a] = min(mn[a], k);
+            mx[a] = max(mx[a], k);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            mn[a] = min(mn[a], __shfl_xor_sync(~0u, mn[a], o));
+            mx[a] = max(mx[a], __shfl_xor_sync(~0u, mx[a], o));
+        }
+        bad = min(bad, __shfl_xor_sync(~0u, bad, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(reinterpret_cast<unsigned long long*>(out + a), mn[a]);
+            atomicMax(reinterpret_cast<unsigned long long*>(out + 3 + a), mx[a]);
+        }
+        if (bad != ~0ull) atomicMin(reinterpret_cast<unsigned long long*>(out + 6), bad);
+    }
+}
+
+__global__ void bbox_init(u64* out) {
+    const int t = threadIdx.x;
+    if (t < 3) out[t] = ~0ull;
+    else if (t < 6) out[t] = 0;
+    else if (t == 6) out[t] = ~0ull;
+}
+
+// ---- K2: quantise + encode, with the 8 byte-digit histograms of the sort fused in --------
+struct EncodeParams {
+    double lo[3];
+    double hi[3];     // closed-box check (sfc.hpp:105)
+    double scale[3];
+    double top;       // 2^level - 1 as double (sfc.hpp:122)
+    int level;
+    int curve;
+    u8 enc[32 * 8];   // Hilbert / Morton encode table (state, octant) -> digit | next << 3
+};
+
+// axis_cell (sfc.hpp:120-124): floor((v - lo) * scale), clamped to [0, top].
+__device__ __forceinline__ u32 axis_cell(double v, double lo, double scale, double top) {
+    double u = floor((v - lo) * scale);
+    u = u < 0.0 ? 0.0 : (top < u ? top : u);
+    return static_cast<u32>(u);
+}
+
+__device__ __forceinline__ u64 encode_cell(u32 cx, u32 cy, u32 cz, int level, int curve,
+                                           const u8* enc) {
+    if (curve == LO_MORTON) return (spread3(cx) << 2) | (spread3(cy) << 1) | spread3(cz);
+    // Hilbert: walk the 24-state descent table from the root (equivalent to the Skilling
+    // transform of sfc.cpp:8-42; pinned by tests against the reference).
+    u64 code = 0;
+    u32 s = 0;
+    for (int d = level - 1; d >= 0; --d) {
+        const u32 g = (((cx >> d) & 1u) << 2) | (((cy >> d) & 1u) << 1) | ((cz >> d) & 1u);
+        const u32 e = enc[s * 8 + g];
+        code = (code << 3) | (e & 7u);
+        s = e >> 3;
+    }
+    return code;
+}
+
+template <bool HIST>
+__global__ void __launch_bounds__(256) encode_kernel(const double* __restrict__ xyz, u64 n,
+                                                     EncodeParams p, u64* __restrict__ codes,
+                                                     u32* __restrict__ hist, u32* __restrict__ err) {
+    __shared__ u8 enc[32 * 8];
+    __shared__ u32 h[HIST ? 8 * 256 : 1];
+    for (int i = threadIdx.x; i < 32 * 8; i += blockDim.x) enc[i] = p.enc[i];
+    if (HIST)
+        for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    u32 outside = 0;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+        if (!(x >= p.lo[0] && x <= p.hi[0] && y >= p.lo[1] && y <= p.hi[1] && z >= p.lo[2] &&
+              z <= p.hi[2]))
+            outside = 1;
+        const u32 cx = axis_cell(x, p.lo[0], p.scale[0], p.top);
+        const u32 cy = axis_cell(y, p.lo[1], p.scale[1], p.top);
+        const u32 cz = axis_cell(z, p.lo[2], p.scale[2], p.top);
+        const u64 code = encode_cell(cx, cy, cz, p.level, p.curve, enc);
+        codes[i] = code;
+        if (HIST) {
+#pragma unroll
+            for (int b = 0; b < 8; ++b) atomicAdd(&h[b * 256 + ((code >> (8 * b)) & 0xff)], 1u);
+        }
+    }
+    if (outside) atomicOr(err, 1u);
+    if (HIST) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x)
+            if (h[i]) atomicAdd(&hist[i], h[i]);
+    }
+}
+
+// ---- K3: onesweep LSD radix sort pass (8-bit digit, stable, decoupled look-back) ---------
+// Tile = 256 threads x 16 keys.  Each warp ranks its 512 keys round by round (lane order
+// within a round, round order within the warp) with __match_any_sync, which keeps equal
+// digits in input order; tiles chain their per-digit totals through a look-back status
+// array (flag in the top 2 bits of a u64 word), so each pass reads and writes every
+// (key, value) exactly once.
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr u64 kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kFlagMask = 3ull << 62;
+
+struct SortSmem {
+    u64 keys[kSortTile];
+    u32 vals[kSortTile];
+    u32 whist[kSortWarps][256];
+    u32 local_start[256];
+    u64 gofs[256];
+    u32 tile;
+    typename cub::BlockScan<u32, kSortThreads>::TempStorage scan;
+};
+
+template <bool FIRST>
+__global__ void __launch_bounds__(kSortThreads, 3) onesweep_pass(
+    const u64* __restrict__ kin, const u32* __restrict__ vin, u64* __restrict__ kout,
+    u32* __restrict__ vout, u64 n, int shift, const u64* __restrict__ digit_base,
+    u64* status, u32* counter) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) S.tile = atomicAdd(counter, 1u);
+    for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&S.whist[0][0])[i] = 0;
+    __syncthreads();
+    const u32 tile = S.tile;
+    const u64 base = static_cast<u64>(tile) * kSortTile;
+    const u64 wbase = base + static_cast<u64>(w) * (32 * kSortItems);
+
+    u64 key[kSortItems];
+    u32 rank[kSortItems];
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const u64 idx = wbase + i * 32 + lane;
+        key[i] = idx < n ? kin[idx] : 0ull;
+    }
+    const u32 lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const bool valid = wbase + i * 32 + lane < n;
+        const u32 d = valid ? static_cast<u32>((key[i] >> shift) & 0xff) : 256u + lane;
+        const u32 peers = __match_any_sync(~0u, d);
+        u32 cnt = 0;
+        if (valid) {
+            cnt = S.whist[w][d];
+            rank[i] = cnt + __popc(peers & lt);
+        }
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) S.whist[w][d] = cnt + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // per digit: exclusive offsets across warps, tile total, look-back for the global prefix
+    const int d = tid;
+    u32 total = 0;
+#pragma unroll
+    for (int ww = 0; ww < kSortWarps; ++ww) {
+        const u32 c = S.whist[ww][d];
+        S.whist[ww][d] = total;
+        total += c;
+    }
+    volatile u64* st = status;
+    st[static_cast<u64>(tile) * 256 + d] = (tile == 0 ? kFlagInc : kFlagAgg) | total;
+    u64 excl = 0;
+    if (tile > 0) {
+        i64 j = static_cast<i64>(tile) - 1;
+        for (;;) {
+            const u64 s = st[static_cast<u64>(j) * 256 + d];
+            const u64 f = s & kFlagMask;
+            if (f == 0) continue;
+            excl += s & ~kFlagMask;
+            if (f == kFlagInc) break;
+            --j;
+        }
+        st[static_cast<u64>(tile) * 256 + d] = kFlagInc | (excl + total);
+    }
+    S.gofs[d] = digit_base[d] + excl;
+    u32 lstart;
+    cub::BlockScan<u32, kSortThreads>(S.scan).ExclusiveSum(total, lstart);
+    S.local_start[d] = lstart;
+    __syncthreads();
+
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const u64 idx = wbase + i * 32 + lane;
+        if (idx < n) {
+            const u32 dd = static_cast<u32>((key[i] >> shift) & 0xff);
+            const u32 pos = S.local_start[dd] + S.whist[w][dd] + rank[i];
+            S.keys[pos] = key[i];
+            S.vals[pos] = FIRST ? static_cast<u32>(idx) : vin[idx];
+        }
+    }
+    __syncthreads();
+    const u64 tile_n = min(static_cast<u64>(kSortTile), n - base);
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const u32 p = i * kSortThreads + tid;
+        if (p < tile_n) {
+            const u64 k = S.keys[p];
+            const u32 dd = static_cast<u32>((k >> shift) & 0xff);
+            const u64 gp = S.gofs[dd] + (p - S.local_start[dd]);
+            kout[gp] = k;
+            vout[gp] = S.vals[p];
+        }
+    }
+}
+
+// ---- K4: gather into SFC order, SoA f64 ---------------------------------------------------
+__global__ void __launch_bounds__(256) gather_soa(const double* __restrict__ xyz,
+                                                  const u32* __restrict__ perm, u64 n,
+                                                  double* __restrict__ x, double* __restrict__ y,
+                                                  double* __restrict__ z) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u64 o = perm[i];
+        x[i] = xyz[3 * o];
+        y[i] = xyz[3 * o + 1];
+        z[i] = xyz[3 * o + 2];
+    }
+}
+
+__global__ void iota_u32(u32* p, u64 n) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x)
+        p[i] = static_cast<u32>(i);
+}
+
+__global__ void interleave_aos(const double* __restrict__ x, const double* __restrict__ y,
+                               const double* __restrict__ z, u64 n, double* __restrict__ xyz) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        xyz[3 * i] = x[i];
+        xyz[3 * i + 1] = y[i];
+        xyz[3 * i + 2] = z[i];
+    }
+}
+
+__global__ void invert_perm_kernel(const u32* __restrict__ perm, u64 n, u32* __restrict__ inv) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x)
+        inv[perm[i]] = static_cast<u32>(i);
+}
+
+__global__ void encode_cells_kernel(const u32* __restrict__ cells, u64 n, int level, int curve,
+                                    EncodeParams p, u64* __restrict__ codes) {
+    __shared__ u8 enc[32 * 8];
+    for (int i = threadIdx.x; i < 32 * 8; i += blockDim.x) enc[i] = p.enc[i];
+    __syncthreads();
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x)
+        codes[i] = encode_cell(cells[3 * i], cells[3 * i + 1], cells[3 * i + 2], level, curve, enc);
+}
+
+__global__ void decode_codes_kernel(const u64* __restrict__ codes, u64 n, int level,
+                                    const CurveTables tab, u32* __restrict__ cells) {
+    __shared__ u8 dec[32 * 8];
+    for (int i = threadIdx.x; i < 32 * 8; i += blockDim.x) dec[i] = tab.dec[i];
+    __syncthreads();
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u64 c = codes[i];
+        u32 x = 0, y = 0, z = 0, s = 0;
+        for (int d = level - 1; d >= 0; --d) {
+            const u32 e = dec[s * 8 + ((c >> (3 * d)) & 7u)];
+            x = x << 1 | ((e >> 2) & 1u);
+            y = y << 1 | ((e >> 1) & 1u);
+            z = z << 1 | (e & 1u);
+            s = e >> 3;
+        }
+        cells[3 * i] = x, cells[3 * i + 1] = y, cells[3 * i + 2] = z;
+    }
+}
+
+static int grid_for(lo_context* ctx, u64 n, int threads, int per_sm = 8) {
+    const u64 want = (n + threads - 1) / threads;
+    const u64 cap = static_cast<u64>(ctx->sm_count) * per_sm;
+    return static_cast<int>(std::max<u64>(1, std::min(want, cap)));
+}
+
+// ---- host: bbox -> Discretizer (cubify, axis_scale) exactly as the reference ------------
+struct Disc {
+    double cloud_box[6];
+    double box[6];
+    double scale[3];
+};
+
+static Disc compute_disc(lo_context* ctx, const double* xyz_dev, u64 n, int level) {
+    u64* bb = dalloc_t<u64>(ctx, 8);
+    bbox_init<<<1, 8, 0, ctx->stream>>>(bb);
+    bbox_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(xyz_dev, n, bb);
+    LO_CHECK_LAUNCH();
+    u64 h[7];
+    LO_CUDA(cudaMemcpyAsync(ctx->pinned_scratch, bb, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    dfree(ctx, bb);
+    sync(ctx);
+    std::memcpy(h, ctx->pinned_scratch, sizeof h);
+    if (h[6] != ~0ull) {
+        throw Error(LO_INVALID_ARGUMENT, "non-finite coordinate at point " + std::to_string(h[6]));
+    }
+    Disc d{};
+    for (int a = 0; a < 6; ++a) d.cloud_box[a] = dbl_from_order_key(h[a]);
+    // cubify (geometry.hpp:47-57): side = max extent, anchored at the min corner
+    const double* b = d.cloud_box;
+    const double side = std::max({b[3] - b[0], b[4] - b[1], b[5] - b[2]});
+    for (int a = 0; a < 3; ++a) {
+        d.box[a] = b[a];
+        d.box[3 + a] = std::max(b[a] + side, b[3 + a]);
+    }
+    // Discretizer ctor (sfc.cpp:99-108) + axis_scale (sfc.cpp:77-80)
+    for (int a = 0; a < 3; ++a) {
+        const double extent = d.box[3 + a] - d.box[a];
+        d.scale[a] = extent > 0.0 ? std::ldexp(1.0, level) / extent : 0.0;
+    }
+    return d;
+}
+
+static EncodeParams make_params(const double box[6], const double scale[3], int level,
+                                int curve) {
+    EncodeParams p{};
+    for (int a = 0; a < 3; ++a) {
+        p.lo[a] = box[a];
+        p.hi[a] = box[3 + a];
+        p.scale[a] = scale[a];
+    }
+    p.top = static_cast<double>((1ull << level) - 1);
+    p.level = level;
+    p.curve = curve;
+    std::memcpy(p.enc, curve_tables(curve).enc, sizeof p.enc);
+    return p;
+}
+
+// Sorts (codes, implicit original index) stably; writes sorted keys + perm.
+static void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int level,
+                       u64* keys_sorted, u32* perm) {
+    const int passes = (3 * level + 7) / 8;
+    // digit bases per pass and the constant-digit skip (reorder.cpp:49)
+    std::vector<int> run;
+    std::vector<u64> bases(8 * 256, 0);
+    for (int p = 0; p < passes; ++p) {
+        bool trivial = false;
+        u64 s = 0;
+        for (int b = 0; b < 256; ++b) {
+            const u32 c = hist_host[p * 256 + b];
+            if (c == n) trivial = true;
+            bases[p * 256 + b] = s;
+            s += c;
+        }
+        if (!trivial) run.push_back(p);
+    }
+    if (run.empty()) {
+        iota_u32<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(perm, n);
+        LO_CHECK_LAUNCH();
+        LO_CUDA(cudaMemcpyAsync(keys_sorted, keys, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        return;
+    }
+    const int tiles = ceil_div(n, kSortTile);
+    u64* dbase = dalloc_t<u64>(ctx, 8 * 256);
+    LO_CUDA(cudaMemcpyAsync(dbase, bases.data(), bases.size() * 8, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    u64* status = dalloc_t<u64>(ctx, static_cast<size_t>(tiles) * 256);
+    u32* counter = dalloc_t<u32>(ctx, 1);
+    u64* kalt = dalloc_t<u64>(ctx, n);
+    u32* valt = dalloc_t<u32>(ctx, n);
+    u32* vtmp = dalloc_t<u32>(ctx, n);
+    // ping-pong so that the final pass lands in (keys_sorted, perm)
+    const int np = static_cast<int>(run.size());
+    const size_t smem = sizeof(SortSmem);
+    static bool attr_set = false;
+    if (!attr_set) {
+        LO_CUDA(cudaFuncSetAttribute(onesweep_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+        LO_CUDA(cudaFuncSetAttribute(onesweep_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+        attr_set = true;
+    }
+    const u64* kin = keys;
+    const u32* vin = nullptr;
+    for (int i = 0; i < np; ++i) {
+        // pass i reads the previous pass's pair; the last pass lands in the outputs
+        const bool last = i == np - 1;
+        u64* kout = last ? keys_sorted : (i % 2 == 0 ? kalt : keys);
+        u32* vout = last ? perm : (i % 2 == 0 ? valt : vtmp);
+        LO_CUDA(cudaMemsetAsync(status, 0, static_cast<size_t>(tiles) * 256 * 8, ctx->stream));
+        LO_CUDA(cudaMemsetAsync(counter, 0, 4, ctx->stream));
+        if (i == 0)
+            onesweep_pass<true><<<tiles, kSortThreads, smem, ctx->stream>>>(
+                kin, nullptr, kout, vout, n, 8 * run[i], dbase + 256 * run[i], status, counter);
+        else
+            onesweep_pass<false><<<tiles, kSortThreads, smem, ctx->stream>>>(
+                kin, vin, kout, vout, n, 8 * run[i], dbase + 256 * run[i], status, counter);
+        LO_CHECK_LAUNCH();
+        kin = kout;
+        vin = vout;
+    }
+    dfree(ctx, dbase);
+    dfree(ctx, status);
+    dfree(ctx, counter);
+    dfree(ctx, kalt);
+    dfree(ctx, valt);
+    dfree(ctx, vtmp);
+}
+
+static lo_coded* reorder_device(lo_context* ctx, const double* xyz, u64 n, int curve, int level) {
+    require(n > 0, LO_INVALID_ARGUMENT, "reorder_cloud: empty cloud");
+    require(n <= 0xffffffffull, LO_INVALID_ARGUMENT,
+            "reorder_cloud: cloud exceeds 32-bit index space");
+    require(level >= 0 && level <= kMaxLevel, LO_INVALID_ARGUMENT, "level out of range");
+    require(curve == LO_MORTON || curve == LO_HILBERT, LO_INVALID_ARGUMENT, "unknown curve");
+    stage_begin(ctx, "bbox");
+    const Disc disc = compute_disc(ctx, xyz, n, level);
+    stage_end(ctx);
+
+    auto* c = new lo_coded;
+    c->ctx = ctx;
+    c->n = n;
+    c->curve = curve;
+    c->level = level;
+    std::memcpy(c->cloud_box, disc.cloud_box, sizeof disc.cloud_box);
+    std::memcpy(c->disc_box, disc.box, sizeof disc.box);
+    std::memcpy(c->scale, disc.scale, sizeof disc.scale);
+    try {
+        stage_begin(ctx, "encode");
+        u64* codes = dalloc_t<u64>(ctx, n);
+        u32* hist = dalloc_t<u32>(ctx, 8 * 256 + 1);
+        LO_CUDA(cudaMemsetAsync(hist, 0, (8 * 256 + 1) * 4, ctx->stream));
+        const EncodeParams p = make_params(disc.box, disc.scale, level, curve);
+        encode_kernel<true><<<grid_for(ctx, n, 256, 4), 256, 0, ctx->stream>>>(
+            xyz, n, p, codes, hist, hist + 8 * 256);
+        LO_CHECK_LAUNCH();
+        stage_end(ctx);
+        std::vector<u32> hh(8 * 256 + 1);
+        LO_CUDA(cudaMemcpyAsync(hh.data(), hist, hh.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        require(hh[8 * 256] == 0, LO_DOMAIN_ERROR, "point outside discretizer bounds");
+
+        stage_begin(ctx, "sort");
+        c->codes = dalloc_t<u64>(ctx, n);
+        c->perm = dalloc_t<u32>(ctx, n);
+        radix_sort(ctx, codes, n, hh.data(), level, c->codes, c->perm);
+        stage_end(ctx);
+        dfree(ctx, codes);
+        dfree(ctx, hist);
+
+        stage_begin(ctx, "gather");
+        c->x = dalloc_t<double>(ctx, n);
+        c->y = dalloc_t<double>(ctx, n);
+        c->z = dalloc_t<double>(ctx, n);
+        gather_soa<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(xyz, c->perm, n, c->x, c->y, c->z);
+        LO_CHECK_LAUNCH();
+        stage_end(ctx);
+        sync(ctx);
+    } catch (...) {
+        dfree(ctx, c->codes);
+        dfree(ctx, c->perm);
+        dfree(ctx, c->x);
+        dfree(ctx, c->y);
+        dfree(ctx, c->z);
+        delete c;
+        throw;
+    }
+    return c;
+}
+
+}  // namespace lo
+
+using namespace lo;
+
+extern "C" {
+
+int lo_compute_codes(lo_context* ctx, const double* xyz_host, uint64_t n, int curve, int level,
+                     const double* disc_box, uint64_t* codes_host) {
+    return api([&] {
+        require(n > 0, LO_INVALID_ARGUMENT, "compute_codes: empty cloud");
+        require(level >= 0 && level <= kMaxLevel, LO_INVALID_ARGUMENT, "level out of range");
+        double* xyz = dalloc_t<double>(ctx, 3 * n);
+        u64* codes = dalloc_t<u64>(ctx, n);
+        u32* err = dalloc_t<u32>(ctx, 1);
+        LO_CUDA(cudaMemsetAsync(err, 0, 4, ctx->stream));
+        LO_CUDA(cudaMemcpyAsync(xyz, xyz_host, 24 * n, cudaMemcpyHostToDevice, ctx->stream));
+        double box[6], scale[3];
+        if (disc_box) {
+            for (int a = 0; a < 3; ++a) {
+                require(disc_box[a] <= disc_box[3 + a], LO_INVALID_ARGUMENT, "inverted bounding box");
+                const double extent = disc_box[3 + a] - disc_box[a];
+                scale[a] = extent > 0.0 ? std::ldexp(1.0, level) / extent : 0.0;
+            }
+            std::memcpy(box, disc_box, sizeof box);
+        } else {
+            const Disc d = compute_disc(ctx, xyz, n, level);
+            std::memcpy(box, d.box, sizeof box);
+            std::memcpy(scale, d.scale, sizeof scale);
+        }
+        const EncodeParams p = make_params(box, scale, level, curve);
+        encode_kernel<false><<<grid_for(ctx, n, 256, 4), 256, 0, ctx->stream>>>(xyz, n, p, codes,
+                                                                                nullptr, err);
+        LO_CHECK_LAUNCH();
+        LO_CUDA(cudaMemcpyAsync(codes_host, codes, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+        const u32 e = read_scalar(ctx, err);
+        dfree(ctx, xyz);
+        dfree(ctx, codes);
+        dfree(ctx, err);
+        sync(ctx);
+        require(e == 0, LO_DOMAIN_ERROR, "point outside discretizer bounds");
+    });
+}
+
+int lo_encode_cells(lo_context* ctx, const uint32_t* cells_host, uint64_t n, int curve, int level,
+                    uint64_t* codes_host) {
+    return api([&] {
+        require(level >= 0 && level <= kMaxLevel, LO_INVALID_ARGUMENT, "level out of range");
+        if (n == 0) return;
+        u32* cells = dalloc_t<u32>(ctx, 3 * n);
+        u64* codes = dalloc_t<u64>(ctx, n);
+        LO_CUDA(cudaMemcpyAsync(cells, cells_host, 12 * n, cudaMemcpyHostToDevice, ctx->stream));
+        const double box[6] = {0, 0, 0, 1, 1, 1}, scale[3] = {0, 0, 0};
+        const EncodeParams p = make_params(box, scale, level, curve);
+        encode_cells_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(cells, n, level, curve,
+                                                                            p, codes);
+        LO_CHECK_LAUNCH();
+        LO_CUDA(cudaMemcpyAsync(codes_host, codes, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+        dfree(ctx, cells);
+        dfree(ctx, codes);
+        sync(ctx);
+    });
+}
+
+int lo_decode_codes(lo_context* ctx, const uint64_t* codes_host, uint64_t n, int curve, int level,
+                    uint32_t* cells_host) {
+    return api([&] {
+        require(level >= 0 && level <= kMaxLevel, LO_INVALID_ARGUMENT, "level out of range");
+        if (n == 0) return;
+        u64* codes = dalloc_t<u64>(ctx, n);
+        u32* cells = dalloc_t<u32>(ctx, 3 * n);
+        LO_CUDA(cudaMemcpyAsync(codes, codes_host, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+        decode_codes_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(
+            codes, n, level, curve_tables(curve), cells);
+        LO_CHECK_LAUNCH();
+        LO_CUDA(cudaMemcpyAsync(cells_host, cells, 12 * n, cudaMemcpyDeviceToHost, ctx->stream));
+        dfree(ctx, codes);
+        dfree(ctx, cells);
+        sync(ctx);
+    });
+}
+
+int lo_reorder_device(lo_context* ctx, const double* xyz_dev, uint64_t n, int curve, int level,
+                      lo_coded** out) {
+    return api([&] { *out = reorder_device(ctx, xyz_dev, n, curve, level); });
+}
+
+int lo_reorder(lo_context* ctx, const double* xyz_host, uint64_t n, int curve, int level,
+               lo_coded** out) {
+    return api([&] {
+        require(n > 0, LO_INVALID_ARGUMENT, "reorder_cloud: empty cloud");
+        double* xyz = dalloc_t<double>(ctx, 3 * n);
+        try {
+            stage_begin(ctx, "h2d");
+            LO_CUDA(cudaMemcpyAsync(xyz, xyz_host, 24 * n, cudaMemcpyHostToDevice, ctx->stream));
+            stage_end(ctx);
+            *out = reorder_device(ctx, xyz, n, curve, level);
+        } catch (...) {
+            dfree(ctx, xyz);
+            throw;
+        }
+        dfree(ctx, xyz);
+    });
+}
+
+int lo_coded_info_get(const lo_coded* c, lo_coded_info* out) {
+    return api([&] {
+        require(c != nullptr, LO_INVALID_ARGUMENT, "null coded cloud");
+        out->n = c->n;
+        out->curve = c->curve;
+        out->level = c->level;
+        std::memcpy(out->disc_box, c->disc_box, sizeof c->disc_box);
+        std::memcpy(out->cloud_box, c->cloud_box, sizeof c->cloud_box);
+        std::memcpy(out->scale, c->scale, sizeof c->scale);
+    });
+}
+
+int lo_coded_download(lo_context* ctx, const lo_coded* c, double* xyz_host, uint64_t* codes_host,
+                      uint32_t* perm_host) {
+    return api([&] {
+        const u64 n = c->n;
+        if (xyz_host) {
+            double* aos = dalloc_t<double>(ctx, 3 * n);
+            interleave_aos<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(c->x, c->y, c->z, n, aos);
+            LO_CHECK_LAUNCH();
+            LO_CUDA(cudaMemcpyAsync(xyz_host, aos, 24 * n, cudaMemcpyDeviceToHost, ctx->stream));
+            dfree(ctx, aos);
+        }
+        if (codes_host)
+            LO_CUDA(cudaMemcpyAsync(codes_host, c->codes, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+        if (perm_host)
+            LO_CUDA(cudaMemcpyAsync(perm_host, c->perm, 4 * n, cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+    });
+}
+
+int lo_coded_device_ptrs(const lo_coded* c, const double** x, const double** y, const double** z,
+                         const uint64_t** codes, const uint32_t** perm) {
+    return api([&] {
+        if (x) *x = c->x;
+        if (y) *y = c->y;
+        if (z) *z = c->z;
+        if (codes) *codes = c->codes;
+        if (perm) *perm = c->perm;
+    });
+}
+
+int lo_coded_destroy(lo_coded* c) {
+    return api([&] {
+        if (!c) return;
+        lo_context* ctx = c->ctx;
+        dfree(ctx, c->x);
+        dfree(ctx, c->y);
+        dfree(ctx, c->z);
+        dfree(ctx, c->codes);
+        dfree(ctx, c->perm);
+        delete c;
+    });
+}
+
+int lo_invert_permutation(lo_context* ctx, const uint32_t* perm_host, uint64_t n, uint32_t* inv_host) {
+    return api([&] {
+        if (n == 0) return;
+        u32* p = dalloc_t<u32>(ctx, n);
+        u32* q = dalloc_t<u32>(ctx, n);
+        LO_CUDA(cudaMemcpyAsync(p, perm_host, 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+        invert_perm_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(p, n, q);
+        LO_CHECK_LAUNCH();
+        LO_CUDA(cudaMemcpyAsync(inv_host, q, 4 * n, cudaMemcpyDeviceToHost, ctx->stream));
+        dfree(ctx, p);
+        dfree(ctx, q);
+        sync(ctx);
+    });
+}
+
+}  // extern "C"
