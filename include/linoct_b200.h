@@ -88,6 +88,8 @@ typedef struct {
 /* ---- context ------------------------------------------------------------------------ */
 const char* lo_last_error(void);
 int lo_abi_version(void);
+/* Number of kernels this library has launched in the process (harness evidence). */
+uint64_t lo_launch_count(void);
 int lo_device_count(int* count);
 /* One context = one device + one CUDA stream.  stream = NULL creates a private stream;
  * otherwise work is enqueued on the given cudaStream_t (e.g. torch's current stream). */
@@ -136,6 +138,9 @@ int lo_coded_download(lo_context* ctx, const lo_coded* coded, double* xyz_host,
 int lo_coded_device_ptrs(const lo_coded* coded, const double** x, const double** y,
                          const double** z, const uint64_t** codes, const uint32_t** perm);
 int lo_coded_destroy(lo_coded* coded);
+/* Multi-GPU replication: an empty CodedCloud with the given header on this context's
+ * device, whose buffers (lo_coded_device_ptrs) are then filled by a broadcast. */
+int lo_coded_create_empty(lo_context* ctx, const lo_coded_info* info, lo_coded** out);
 /* invert_permutation (reorder.hpp:36) */
 int lo_invert_permutation(lo_context* ctx, const uint32_t* perm_host, uint64_t n,
                           uint32_t* inv_host);
@@ -156,6 +161,12 @@ int lo_octree_download(lo_context* ctx, const lo_octree* tree, uint64_t* boundar
 int lo_octree_node_bounds(lo_context* ctx, const lo_octree* tree, const int32_t* refs_host,
                           uint64_t count, double* boxes_host);
 int lo_octree_destroy(lo_octree* tree);
+/* Device buffers of a tree (boundaries u64[L+1], offsets u32[L+1], nodes[I], traversal
+ * table tnodes*64 bytes) and an empty tree of the same shape for replication. */
+int lo_octree_device_ptrs(const lo_octree* tree, void** boundaries, void** offsets, void** nodes,
+                          void** tnodes);
+int lo_octree_create_empty(lo_context* ctx, const lo_coded* coded, const lo_octree_info* info,
+                           lo_octree** out);
 
 /* ---- radius search (search.cpp:45-156, :261-351) ------------------------------------ */
 /* run_radius_batch(tree, coded, method, shape, radius, options).  centres_host == NULL is
@@ -168,6 +179,11 @@ int lo_radius(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int
  * centres, search.hpp:61-64): queries_host is AoS f64, m*3. */
 int lo_radius_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int shape,
                      double radius, const double* queries_host, uint64_t m, lo_csr** out);
+/* Full mode restricted to the contiguous centre range [begin, end) (a shard of the
+ * SFC-ordered queries); row r is centre begin + r, indices stay global. */
+int lo_radius_range(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int method,
+                    int shape, double radius, uint64_t begin, uint64_t end, int fingerprint,
+                    lo_csr** out);
 int lo_csr_info_get(const lo_csr* csr, lo_csr_info* out);
 /* counts[m], fingerprints[m] (FNV-1a-64, search.cpp:263-271), offsets[m+1], indices[total]. */
 int lo_csr_download(lo_context* ctx, const lo_csr* csr, uint32_t* counts_host,
@@ -183,6 +199,9 @@ int lo_knn(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32
 /* knn_lin_oct(tree, coded, Point, k) at arbitrary centres (search.hpp:101-105). */
 int lo_knn_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32_t k,
                   const double* queries_host, uint64_t m, lo_knn_result** out);
+/* Full mode over the contiguous centre range [begin, end). */
+int lo_knn_range(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32_t k,
+                 uint64_t begin, uint64_t end, int fingerprint, lo_knn_result** out);
 /* rows, k_eff (= min(k, N)), device ms */
 int lo_knn_info_get(const lo_knn_result* res, uint64_t* rows, uint32_t* k_eff, double* device_ms);
 /* idx[m*k_eff], dist[m*k_eff], fingerprints[m]; NULL skips. */

@@ -307,6 +307,20 @@ class RefPipeline:
         self.ref.L.ref_radius_point(self.h, shape, _ptr(c), r, _ptr(out), cnt)
         return out
 
+    def radius_range(self, r, begin, end, shape=0, method=1, threads=None, digests=True):
+        """neighbours_lin over the sorted centres [begin, end); returns (wall s, counts, fps)."""
+        m = end - begin
+        counts = np.empty(m, np.uint32)
+        fps = np.empty(m, np.uint64) if digests else None
+        wall = self.ref.L.ref_radius_range(self.h, method, shape, r, begin, end,
+                                           threads or self.threads, _ptr(counts), _ptr(fps))
+        return wall, counts, fps
+
+    def knn_range(self, k, begin, end, threads=None, digests=True):
+        fps = np.empty(end - begin, np.uint64) if digests else None
+        wall = self.ref.L.ref_knn_range(self.h, k, begin, end, threads or self.threads, _ptr(fps))
+        return wall, fps
+
     def locality(self, k, use_perm_map=False, threads=None):
         L = self.ref.L
         th = threads or self.threads
@@ -357,6 +371,10 @@ class Ref:
         L.ref_radius_point.restype = i64
         L.ref_locality.argtypes = [P, u32, C.c_int, C.c_int, P, P, u64]
         L.ref_locality.restype = i64
+        L.ref_radius_range.argtypes = [P, C.c_int, C.c_int, f64, u64, u64, C.c_int, P, P]
+        L.ref_radius_range.restype = f64
+        L.ref_knn_range.argtypes = [P, u32, u64, u64, C.c_int, P]
+        L.ref_knn_range.restype = f64
 
     def max_threads(self):
         return self.L.ref_max_threads()

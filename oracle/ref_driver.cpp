@@ -329,3 +329,61 @@ std::int64_t ref_locality(void* h, std::uint32_t k, int threads, int use_perm_ma
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// The reference's own per-centre search (neighbours_lin / neighbours_prune,
+// search.hpp:61-71) over the contiguous SFC-ordered centre range [begin, end), with the
+// batch loop's dynamic OpenMP schedule and FNV digests (search.cpp:287-312, :345-347).
+// This is run_batch_loop restricted to a slice, used for bounded CPU-baseline samples.
+// Returns wall seconds of the loop (steady_clock, as run_batch_loop measures).
+double ref_radius_range(void* h, int method, int shape, double radius, std::uint64_t begin,
+                        std::uint64_t end, int threads, std::uint32_t* counts, std::uint64_t* fps) {
+    auto* p = static_cast<Pipeline*>(h);
+    const std::int64_t m = static_cast<std::int64_t>(end - begin);
+    const auto t0 = std::chrono::steady_clock::now();
+#pragma omp parallel for schedule(dynamic) num_threads(threads)
+    for (std::int64_t i = 0; i < m; ++i) {
+        thread_local std::vector<std::uint32_t> idx;
+        const SearchKernel kernel(static_cast<KernelShape>(shape),
+                                  p->coded.cloud[begin + static_cast<std::uint64_t>(i)], radius);
+        if (method == 2) neighbours_prune(*p->tree, p->coded, kernel, idx);
+        else neighbours_lin(*p->tree, p->coded, kernel, idx);
+        std::uint64_t hsh = 0xcbf29ce484222325ULL;
+        for (std::uint32_t v : idx) {
+            for (int b = 0; b < 8; ++b) {
+                hsh ^= (static_cast<std::uint64_t>(v) >> (8 * b)) & 0xff;
+                hsh *= 0x100000001b3ULL;
+            }
+        }
+        if (counts) counts[i] = static_cast<std::uint32_t>(idx.size());
+        if (fps) fps[i] = hsh;
+    }
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// knn_lin_oct over [begin, end) (search.cpp:369-388 restricted to a slice).
+double ref_knn_range(void* h, std::uint32_t k, std::uint64_t begin, std::uint64_t end, int threads,
+                     std::uint64_t* fps) {
+    auto* p = static_cast<Pipeline*>(h);
+    const std::int64_t m = static_cast<std::int64_t>(end - begin);
+    const auto t0 = std::chrono::steady_clock::now();
+#pragma omp parallel for schedule(dynamic) num_threads(threads)
+    for (std::int64_t i = 0; i < m; ++i) {
+        thread_local std::vector<KnnNeighbor> found;
+        knn_lin_oct(*p->tree, p->coded, p->coded.cloud[begin + static_cast<std::uint64_t>(i)], k, found);
+        std::uint64_t hsh = 0xcbf29ce484222325ULL;
+        for (const KnnNeighbor& nb : found) {
+            const std::uint64_t vals[2] = {nb.index, std::bit_cast<std::uint64_t>(nb.dist_sq)};
+            for (std::uint64_t v : vals)
+                for (int b = 0; b < 8; ++b) {
+                    hsh ^= (v >> (8 * b)) & 0xff;
+                    hsh *= 0x100000001b3ULL;
+                }
+        }
+        if (fps) fps[i] = hsh;
+    }
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // extern "C"

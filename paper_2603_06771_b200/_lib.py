@@ -37,6 +37,7 @@ class CsrInfo(C.Structure):
 SIGNATURES = {
     "lo_last_error": (C.c_char_p, []),
     "lo_abi_version": (cint, []),
+    "lo_launch_count": (u64, []),
     "lo_device_count": (cint, [P]),
     "lo_context_create": (cint, [cint, P, PP]),
     "lo_context_destroy": (cint, [P]),
@@ -60,6 +61,7 @@ SIGNATURES = {
     "lo_coded_download": (cint, [P, P, P, P, P]),
     "lo_coded_device_ptrs": (cint, [P, PP, PP, PP, PP, PP]),
     "lo_coded_destroy": (cint, [P]),
+    "lo_coded_create_empty": (cint, [P, C.POINTER(CodedInfo), PP]),
     "lo_invert_permutation": (cint, [P, P, u64, P]),
     "lo_build_leaves": (cint, [P, P, u64, u32, cint, P, P, P, u64]),
     "lo_octree_build": (cint, [P, P, u32, PP]),
@@ -67,14 +69,18 @@ SIGNATURES = {
     "lo_octree_download": (cint, [P, P, P, P, P]),
     "lo_octree_node_bounds": (cint, [P, P, P, u64, P]),
     "lo_octree_destroy": (cint, [P]),
+    "lo_octree_device_ptrs": (cint, [P, PP, PP, PP, PP]),
+    "lo_octree_create_empty": (cint, [P, P, C.POINTER(OctreeInfo), PP]),
     "lo_radius": (cint, [P, P, P, cint, cint, f64, P, u64, cint, PP]),
     "lo_radius_points": (cint, [P, P, P, cint, f64, P, u64, PP]),
+    "lo_radius_range": (cint, [P, P, P, cint, cint, f64, u64, u64, cint, PP]),
     "lo_csr_info_get": (cint, [P, C.POINTER(CsrInfo)]),
     "lo_csr_download": (cint, [P, P, P, P, P, P]),
     "lo_csr_device_ptrs": (cint, [P, PP, PP]),
     "lo_csr_destroy": (cint, [P]),
     "lo_knn": (cint, [P, P, P, u32, P, u64, cint, PP]),
     "lo_knn_points": (cint, [P, P, P, u32, P, u64, PP]),
+    "lo_knn_range": (cint, [P, P, P, u32, u64, u64, cint, PP]),
     "lo_knn_info_get": (cint, [P, P, P, P]),
     "lo_knn_download": (cint, [P, P, P, P, P]),
     "lo_knn_destroy": (cint, [P]),

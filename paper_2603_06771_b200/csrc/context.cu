@@ -3,6 +3,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <mutex>
 
@@ -12,6 +13,9 @@ namespace lo {
 
 thread_local std::string g_last_error;
 void set_last_error(const char* m) { g_last_error = m; }
+
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
     char buf[512];
@@ -295,6 +299,7 @@ using namespace lo;
 extern "C" {
 
 const char* lo_last_error(void) { return g_last_error.c_str(); }
+uint64_t lo_launch_count(void) { return g_launches.load(); }
 int lo_abi_version(void) { return LO_ABI_VERSION; }
 
 int lo_device_count(int* count) {

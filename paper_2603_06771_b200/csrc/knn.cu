@@ -357,6 +357,17 @@ int lo_knn_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded,
     });
 }
 
+int lo_knn_range(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32_t k,
+                 uint64_t begin, uint64_t end, int fingerprint, lo_knn_result** out) {
+    return api([&] {
+        require(k >= 1, LO_INVALID_ARGUMENT, "knn: k must be >= 1");
+        require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
+        require(begin <= end && end <= coded->n, LO_INVALID_ARGUMENT, "centre range out of bounds");
+        Queries q{coded->x + begin, coded->y + begin, coded->z + begin, nullptr, end - begin};
+        *out = knn_search(ctx, tree, coded, k, q, fingerprint != 0);
+    });
+}
+
 int lo_knn_info_get(const lo_knn_result* res, uint64_t* rows, uint32_t* k_eff, double* device_ms) {
     return api([&] {
         if (rows) *rows = res->rows;

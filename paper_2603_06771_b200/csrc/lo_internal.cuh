@@ -37,7 +37,14 @@ struct Error : std::runtime_error {
         cudaError_t e_ = (call);                                               \
         if (e_ != cudaSuccess) ::lo::throw_cuda(e_, #call, __FILE__, __LINE__); \
     } while (0)
-#define LO_CHECK_LAUNCH() LO_CUDA(cudaGetLastError())
+// Every kernel launch is followed by exactly one LO_CHECK_LAUNCH(), which also counts it
+// (lo_launch_count(): the harness's evidence of how many of our kernels ran).
+void count_launch();
+#define LO_CHECK_LAUNCH()                 \
+    do {                                  \
+        LO_CUDA(cudaGetLastError());      \
+        ::lo::count_launch();             \
+    } while (0)
 
 inline void require(bool ok, int status, const std::string& msg) {
     if (!ok) throw Error(status, msg);

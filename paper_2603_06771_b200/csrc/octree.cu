@@ -511,6 +511,48 @@ int lo_octree_node_bounds(lo_context* ctx, const lo_octree* t, const int32_t* re
     });
 }
 
+int lo_octree_device_ptrs(const lo_octree* t, void** boundaries, void** offsets, void** nodes,
+                          void** tnodes) {
+    return api([&] {
+        if (boundaries) *boundaries = t->bounds;
+        if (offsets) *offsets = t->offsets;
+        if (nodes) *nodes = t->nodes;
+        if (tnodes) *tnodes = t->tn;
+    });
+}
+
+int lo_octree_create_empty(lo_context* ctx, const lo_coded* coded, const lo_octree_info* info,
+                           lo_octree** out) {
+    return api([&] {
+        require(coded && info && info->points == coded->n, LO_INVALID_ARGUMENT,
+                "octree header does not match the coded cloud");
+        auto* t = new lo_octree;
+        t->ctx = ctx;
+        t->coded = coded;
+        t->points = info->points;
+        t->leaves = info->leaves;
+        t->internal = info->internal;
+        t->tnodes = info->tnodes;
+        t->root = info->root;
+        t->n_max = info->n_max;
+        t->level = info->level;
+        t->curve = info->curve;
+        std::memcpy(t->disc_box, coded->disc_box, sizeof t->disc_box);
+        try {
+            t->bounds = dalloc_t<u64>(ctx, t->leaves + 1);
+            t->offsets = dalloc_t<u32>(ctx, t->leaves + 1);
+            t->nodes = dalloc_t<lo_internal_node>(ctx, t->internal);
+            t->tn = dalloc_t<TNode>(ctx, t->tnodes);
+            sync(ctx);
+        } catch (...) {
+            dfree(ctx, t->bounds), dfree(ctx, t->offsets), dfree(ctx, t->nodes), dfree(ctx, t->tn);
+            delete t;
+            throw;
+        }
+        *out = t;
+    });
+}
+
 int lo_octree_destroy(lo_octree* t) {
     return api([&] {
         if (!t) return;

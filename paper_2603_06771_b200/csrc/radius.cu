@@ -256,6 +256,19 @@ int lo_radius_points(lo_context* ctx, const lo_octree* tree, const lo_coded* cod
     });
 }
 
+int lo_radius_range(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int method,
+                    int shape, double radius, uint64_t begin, uint64_t end, int fingerprint,
+                    lo_csr** out) {
+    return api([&] {
+        require(method == LO_METHOD_LIN || method == LO_METHOD_PRUNE || method == LO_METHOD_STRUCT,
+                LO_INVALID_ARGUMENT, "unknown radius method");
+        require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
+        require(begin <= end && end <= coded->n, LO_INVALID_ARGUMENT, "centre range out of bounds");
+        Queries q{coded->x + begin, coded->y + begin, coded->z + begin, nullptr, end - begin};
+        *out = radius_search(ctx, tree, coded, shape, radius, q, fingerprint != 0);
+    });
+}
+
 int lo_csr_info_get(const lo_csr* csr, lo_csr_info* out) {
     return api([&] {
         out->rows = csr->rows;

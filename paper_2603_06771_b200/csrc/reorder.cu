@@ -322,6 +322,7 @@ struct Disc {
 static Disc compute_disc(lo_context* ctx, const double* xyz_dev, u64 n, int level) {
     u64* bb = dalloc_t<u64>(ctx, 8);
     bbox_init<<<1, 8, 0, ctx->stream>>>(bb);
+    LO_CHECK_LAUNCH();
     bbox_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(xyz_dev, n, bb);
     LO_CHECK_LAUNCH();
     u64 h[7];
@@ -652,6 +653,34 @@ int lo_coded_destroy(lo_coded* c) {
         dfree(ctx, c->codes);
         dfree(ctx, c->perm);
         delete c;
+    });
+}
+
+int lo_coded_create_empty(lo_context* ctx, const lo_coded_info* info, lo_coded** out) {
+    return api([&] {
+        require(info && info->n > 0 && info->n <= 0xffffffffull, LO_INVALID_ARGUMENT,
+                "coded cloud header: bad size");
+        auto* c = new lo_coded;
+        c->ctx = ctx;
+        c->n = info->n;
+        c->curve = info->curve;
+        c->level = info->level;
+        std::memcpy(c->disc_box, info->disc_box, sizeof c->disc_box);
+        std::memcpy(c->cloud_box, info->cloud_box, sizeof c->cloud_box);
+        std::memcpy(c->scale, info->scale, sizeof c->scale);
+        try {
+            c->x = dalloc_t<double>(ctx, c->n);
+            c->y = dalloc_t<double>(ctx, c->n);
+            c->z = dalloc_t<double>(ctx, c->n);
+            c->codes = dalloc_t<u64>(ctx, c->n);
+            c->perm = dalloc_t<u32>(ctx, c->n);
+            sync(ctx);
+        } catch (...) {
+            dfree(ctx, c->x), dfree(ctx, c->y), dfree(ctx, c->z), dfree(ctx, c->codes), dfree(ctx, c->perm);
+            delete c;
+            throw;
+        }
+        *out = c;
     });
 }
 

@@ -1,0 +1,124 @@
+"""Multi-GPU plumbing (one process per GPU, torch.distributed over NCCL / NVLink).
+
+SURVEY.md §8e: the sorted points and the octree are built once (rank `src`) and broadcast;
+queries shard by contiguous SFC-ordered index ranges; each rank's CSR rows are global rows
+[begin, end) and are concatenated by offset -- the only other exchange is one all-gather of
+the per-rank neighbour totals.  No collective sits on the search path itself.
+
+The tensor-level helpers (`shard_range`, `global_row_base`, `broadcast_buffers`) take plain
+torch tensors, so the same code runs with gloo on CPU (tests/test_distributed.py) and NCCL on
+device memory views of the library's buffers (`device_view`).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from ._lib import CodedInfo, OctreeInfo, check
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced split of [0, n): rank r owns [r*n//w, (r+1)*n//w)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def weighted_shard_range(prefix: np.ndarray, rank: int, world: int) -> tuple[int, int]:
+    """Split rows so each rank gets ~equal work, given an inclusive-prefix-style array of
+    per-row cost with prefix[0] = 0 and prefix[-1] = total (e.g. CSR offsets after a count
+    pass): the fill pass of cfg3 is balanced by neighbours, not by queries (§8e.3)."""
+    total = int(prefix[-1])
+    lo = int(np.searchsorted(prefix, total * rank // world, side="left"))
+    hi = int(np.searchsorted(prefix, total * (rank + 1) // world, side="left"))
+    if rank == world - 1:
+        hi = len(prefix) - 1
+    return min(lo, len(prefix) - 1), min(hi, len(prefix) - 1)
+
+
+def global_row_base(local_total: int, group=None, device=None) -> tuple[int, int]:
+    """Exclusive prefix of the per-rank totals (u64) -> (this rank's base, grand total)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    t = torch.tensor([local_total], dtype=torch.int64, device=device)
+    gathered = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(gathered, t, group=group)
+    vals = [int(g.item()) for g in gathered]
+    return sum(vals[:rank]), sum(vals)
+
+
+def broadcast_buffers(buffers: list[torch.Tensor], src: int = 0, group=None) -> None:
+    """Broadcast every tensor in place from `src` (uint8 views of device memory under NCCL)."""
+    for b in buffers:
+        if b.numel():
+            dist.broadcast(b, src=src, group=group)
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ wrapper so torch can view library-owned memory."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 2,
+            "strides": None,
+        }
+
+
+def device_view(ptr: int, nbytes: int, device: int) -> torch.Tensor:
+    """Zero-copy uint8 tensor over `nbytes` of device memory at `ptr`."""
+    if nbytes == 0:
+        return torch.empty(0, dtype=torch.uint8, device=f"cuda:{device}")
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CudaArray(ptr, nbytes), device=f"cuda:{device}")
+
+
+def _coded_views(coded_h, n: int, device: int) -> list[torch.Tensor]:
+    L = _lib.lib()
+    x, y, z, codes, perm = (C.c_void_p() for _ in range(5))
+    check(L.lo_coded_device_ptrs(coded_h, C.byref(x), C.byref(y), C.byref(z), C.byref(codes),
+                                 C.byref(perm)))
+    return [device_view(x.value, 8 * n, device), device_view(y.value, 8 * n, device),
+            device_view(z.value, 8 * n, device), device_view(codes.value, 8 * n, device),
+            device_view(perm.value, 4 * n, device)]
+
+
+def _tree_views(tree_h, info: OctreeInfo, device: int) -> list[torch.Tensor]:
+    L = _lib.lib()
+    b, o, nodes, tn = (C.c_void_p() for _ in range(4))
+    check(L.lo_octree_device_ptrs(tree_h, C.byref(b), C.byref(o), C.byref(nodes), C.byref(tn)))
+    return [device_view(b.value, 8 * (info.leaves + 1), device),
+            device_view(o.value, 4 * (info.leaves + 1), device),
+            device_view(nodes.value, 56 * info.internal, device),
+            device_view(tn.value, 64 * info.tnodes, device)]
+
+
+def broadcast_structure(ctx, coded_h, tree_h, src: int = 0, group=None):
+    """Replicate (CodedCloud, LinearOctree) from rank `src` to every rank of `group`.
+
+    Rank src passes its handles; the others pass None and receive new handles.  Returns
+    (coded_h, tree_h, coded_info, tree_info) on every rank."""
+    rank = dist.get_rank(group)
+    L = _lib.lib()
+    header = [None]
+    if rank == src:
+        ci, ti = CodedInfo(), OctreeInfo()
+        check(L.lo_coded_info_get(coded_h, C.byref(ci)))
+        check(L.lo_octree_info_get(tree_h, C.byref(ti)))
+        header = [(bytes(ci), bytes(ti))]
+    dist.broadcast_object_list(header, src=src, group=group)
+    ci = CodedInfo.from_buffer_copy(header[0][0])
+    ti = OctreeInfo.from_buffer_copy(header[0][1])
+    if rank != src:
+        h = C.c_void_p()
+        check(L.lo_coded_create_empty(ctx.h, C.byref(ci), C.byref(h)))
+        coded_h = h
+        t = C.c_void_p()
+        check(L.lo_octree_create_empty(ctx.h, coded_h, C.byref(ti), C.byref(t)))
+        tree_h = t
+    ctx.synchronize()
+    views = _coded_views(coded_h, ci.n, ctx.device) + _tree_views(tree_h, ti, ctx.device)
+    broadcast_buffers(views, src=src, group=group)
+    torch.cuda.synchronize(ctx.device)
+    return coded_h, tree_h, ci, ti
