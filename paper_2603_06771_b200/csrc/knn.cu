@@ -16,8 +16,8 @@
 namespace lo {
 
 u32* upload_centres(lo_context* ctx, const u32* centres_host, u64 m, u64 n);
-void upload_points(lo_context* ctx, const double* xyz_host, u64 m, double** x, double** y,
-                   double** z);
+void upload_points(lo_context* ctx, const lo_coded* c, const double* xyz_host, u64 m, double** x,
+                   double** y, double** z, float4** f, double* bmax);
 
 // (a.d, a.i) > (b.d, b.i) lexicographically: heap_after (search.cpp:173-177) on points.
 __device__ __forceinline__ bool after(double ad, u32 ai, double bd, u32 bi) {
@@ -344,16 +344,19 @@ int lo_knn_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded,
                   const double* queries_host, uint64_t m, lo_knn_result** out) {
     return api([&] {
         require(k >= 1, LO_INVALID_ARGUMENT, "knn: k must be >= 1");
-        double *x = nullptr, *y = nullptr, *z = nullptr;
-        if (m) upload_points(ctx, queries_host, m, &x, &y, &z);
-        Queries q{x, y, z, nullptr, m};
+        require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
+        ensure_float_shadows(ctx, coded, tree);
+        double *x = nullptr, *y = nullptr, *z = nullptr, bmax = 0.0;
+        float4* f = nullptr;
+        if (m) upload_points(ctx, coded, queries_host, m, &x, &y, &z, &f, &bmax);
+        Queries q{x, y, z, nullptr, m, f, bmax};
         try {
             *out = knn_search(ctx, tree, coded, k, q, true);
         } catch (...) {
-            dfree(ctx, x), dfree(ctx, y), dfree(ctx, z);
+            dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f);
             throw;
         }
-        dfree(ctx, x), dfree(ctx, y), dfree(ctx, z);
+        dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f);
     });
 }
 

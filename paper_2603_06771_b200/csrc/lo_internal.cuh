@@ -73,6 +73,16 @@ struct __align__(16) TNode {
 };
 static_assert(sizeof(TNode) == 64, "TNode must be 64 bytes");
 
+// FP32 shadow of a TNode for the filtered search: the box relative to the cloud origin,
+// rounded outward (directed rounding), so it still contains every point's exact relative
+// position.  a = (lo.xyz, begin bits), b = (hi.xyz, end bits), c = (child0, nchild, -, -).
+struct __align__(16) TNodeF {
+    float4 a;
+    float4 b;
+    uint4 c;
+};
+static_assert(sizeof(TNodeF) == 48, "TNodeF must be 48 bytes");
+
 }  // namespace lo
 
 struct lo_context {
@@ -100,6 +110,10 @@ struct lo_coded {
     double *x = nullptr, *y = nullptr, *z = nullptr;  // sorted SoA coordinates
     lo::u64* codes = nullptr;                         // sorted codes
     lo::u32* perm = nullptr;                          // perm[new] = old
+    // FP32 filter copy: fl32(fl64(p - origin)), origin = disc box min (search_common.cuh)
+    float4* pf = nullptr;
+    double origin[3] = {};
+    double bmax = 0.0;  // >= |p - origin| on every axis (the cube side)
 };
 
 struct lo_octree {
@@ -114,8 +128,14 @@ struct lo_octree {
     lo::u32* offsets = nullptr;         // [leaves+1]
     lo_internal_node* nodes = nullptr;  // [internal]
     lo::TNode* tn = nullptr;            // [tnodes]
+    lo::TNodeF* tf = nullptr;           // [tnodes] FP32 shadow (built lazily for replicas)
     int max_depth = 0;
 };
+
+namespace lo {
+// Lazily (re)build the FP32 shadows (after a broadcast the replicas only hold the exact data).
+void ensure_float_shadows(lo_context* ctx, const lo_coded* coded, const lo_octree* tree);
+}  // namespace lo
 
 struct lo_csr {
     lo_context* ctx = nullptr;

@@ -235,6 +235,47 @@ __global__ void tnode_boxes(TNode* tn, u64 tnodes, const double* __restrict__ x,
     }
 }
 
+// FP32 shadow of the traversal table: boxes relative to the cloud origin rounded outward
+// (directed-rounding subtract, then directed-rounding narrowing), so they keep containing
+// every point's exact relative position.
+__global__ void tnode_float(const TNode* __restrict__ tn, u64 T, TNodeF* __restrict__ tf,
+                            double ox, double oy, double oz) {
+    for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < T;
+         t += (u64)gridDim.x * blockDim.x) {
+        const TNode nd = tn[t];
+        const double o[3] = {ox, oy, oz};
+        float lo[3], hi[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = __double2float_rd(__dsub_rd(nd.lo[a], o[a]));
+            hi[a] = __double2float_ru(__dsub_ru(nd.hi[a], o[a]));
+        }
+        TNodeF f;
+        f.a = make_float4(lo[0], lo[1], lo[2], __uint_as_float(nd.begin));
+        f.b = make_float4(hi[0], hi[1], hi[2], __uint_as_float(nd.end));
+        f.c = make_uint4(nd.child0, nd.nchild, 0u, 0u);
+        tf[t] = f;
+    }
+}
+
+void build_float_points(lo_context* ctx, lo_coded* c);  // reorder.cu
+
+static void build_float_nodes(lo_context* ctx, lo_octree* t, const lo_coded* c) {
+    if (t->tf) return;
+    t->tf = dalloc_t<TNodeF>(ctx, t->tnodes);
+    const int g = static_cast<int>(std::max<u64>(1, std::min<u64>((t->tnodes + 255) / 256,
+                                                                  ctx->sm_count * 16ull)));
+    tnode_float<<<g, 256, 0, ctx->stream>>>(t->tn, t->tnodes, t->tf,
+                                                                 c->origin[0], c->origin[1],
+                                                                 c->origin[2]);
+    LO_CHECK_LAUNCH();
+}
+
+void ensure_float_shadows(lo_context* ctx, const lo_coded* coded, const lo_octree* tree) {
+    build_float_points(ctx, const_cast<lo_coded*>(coded));
+    build_float_nodes(ctx, const_cast<lo_octree*>(tree), coded);
+}
+
 // node_bounds (linear_octree.cpp:139-147): padded octant box of a NodeRef.
 struct BoundsParams {
     double box[6];
@@ -400,6 +441,7 @@ static lo_octree* octree_build(lo_context* ctx, const lo_coded* coded, u32 n_max
     tnode_boxes<<<grid1(ctx, T, 128), 128, 0, ctx->stream>>>(t->tn, T, coded->x, coded->y,
                                                               coded->z, parent, tid_of, arrivals);
     LO_CHECK_LAUNCH();
+    build_float_nodes(ctx, t, coded);
     stage_end(ctx);
     dfree(ctx, tbase);
     dfree(ctx, parent);
@@ -561,6 +603,7 @@ int lo_octree_destroy(lo_octree* t) {
         dfree(ctx, t->offsets);
         dfree(ctx, t->nodes);
         dfree(ctx, t->tn);
+        dfree(ctx, t->tf);
         delete t;
     });
 }

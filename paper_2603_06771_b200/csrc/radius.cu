@@ -86,6 +86,104 @@ __global__ void __launch_bounds__(kRadiusThreads) radius_kernel(
     }
 }
 
+// Same walk with the FP32 filter (search_common.cuh): node relations and point tests run in
+// FP32 with rigorous margins; only points inside the uncertainty band re-run the exact FP64
+// predicate, so the index sets are the reference's bit for bit.
+template <int SHAPE, bool FILL>
+__global__ void __launch_bounds__(kRadiusThreads, 8) radius_float_kernel(
+    const TNodeF* __restrict__ tf, const float4* __restrict__ pf, const double* __restrict__ px,
+    const double* __restrict__ py, const double* __restrict__ pz, Queries q, FloatTest ft,
+    double r, double r2, u32* __restrict__ counts, const u64* __restrict__ offsets,
+    u32* __restrict__ out, u64* tile_counter) {
+    __shared__ u32 stack_s[kRadiusWarps][kStackCap];
+    __shared__ float4 sp_s[kRadiusWarps][32];
+    __shared__ float4 sq_s[kRadiusWarps][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    u32* stack = stack_s[w];
+    float4* spts = sp_s[w];
+    float4* squeries = sq_s[w];
+    const u64 ntiles = (q.m + 31) / 32;
+    const int cl = lane & 7, grp = lane >> 3;
+    for (;;) {
+        // dynamic tile scheduling: heavy tiles (dense clusters) do not stall a static stride
+        u64 tile = 0;
+        if (lane == 0) tile = atomicAdd(reinterpret_cast<unsigned long long*>(tile_counter), 1ull);
+        tile = __shfl_sync(~0u, tile, 0);
+        if (tile >= ntiles) break;
+        const u64 qi = tile * 32 + lane;
+        const bool active = qi < q.m;
+        double cx = 0.0, cy = 0.0, cz = 0.0;
+        float4 qf = make_float4(INFINITY, INFINITY, INFINITY, 0.f);  // never near anything
+        if (active) {
+            load_query(q, qi, cx, cy, cz);
+            qf = load_query_f(q, qi);
+        }
+        __syncwarp();
+        squeries[lane] = qf;
+        u32 count = 0;
+        u32* row = nullptr;
+        if (FILL && active) row = out + offsets[qi];
+        int sp = 1;
+        if (lane == 0) stack[0] = 0;
+        __syncwarp();
+        while (sp > 0) {
+            const u32 t = stack[--sp];
+            const NodeF nd = load_node_f(tf, t);
+            if (nd.nchild != 0) {
+                // internal: lane (child cl, query group grp) tests child cl against the 8
+                // queries of its group; a child is kept when any of the 32 queries may reach it
+                bool keep = false;
+                if (cl < static_cast<int>(nd.nchild)) {
+                    const NodeF ch = load_node_f(tf, nd.child0 + cl);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) keep |= !disjoint_f<SHAPE>(squeries[8 * grp + j], ch, ft);
+                }
+                u32 s = __ballot_sync(~0u, keep);
+                s = (s | (s >> 8) | (s >> 16) | (s >> 24)) & 0xffu;
+                const int k = __popc(s);
+                __syncwarp();
+                if (lane < 8 && ((s >> lane) & 1u))
+                    stack[sp + k - 1 - __popc(s & ((1u << lane) - 1u))] = nd.child0 + lane;
+                sp += k;
+                __syncwarp();
+                continue;
+            }
+            int rel = kDisjoint;
+            if (active) rel = relation_f<SHAPE>(qf, nd, ft);
+            if (rel == kContains) {
+                if (FILL)
+                    for (u32 i = nd.begin; i < nd.end; ++i) row[count + (i - nd.begin)] = i;
+                count += nd.end - nd.begin;
+            }
+            if (!__ballot_sync(~0u, rel == kIntersects)) continue;
+            {
+                for (u32 base = nd.begin; base < nd.end; base += 32) {
+                    const u32 j = base + lane;
+                    __syncwarp();
+                    if (j < nd.end) spts[lane] = __ldg(pf + j);
+                    __syncwarp();
+                    if (rel == kIntersects) {
+                        const u32 cnt = min(32u, nd.end - base);
+                        for (u32 jj = 0; jj < cnt; ++jj) {
+                            int c = classify_f<SHAPE>(qf, spts[jj], ft);
+                            if (c == 2) {
+                                const u32 g = base + jj;
+                                c = contains<SHAPE>(cx, cy, cz, r, r2, px[g], py[g], pz[g]) ? 1 : 0;
+                            }
+                            if (c) {
+                                if (FILL) row[count] = base + jj;
+                                ++count;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (!FILL && active) counts[qi] = count;
+        __syncwarp();
+    }
+}
+
 // K8: FNV-1a-64 per row over its indices (search.cpp:345-347).
 __global__ void radius_digest(const u64* __restrict__ offsets, const u32* __restrict__ idx, u64 m,
                               u64* __restrict__ fps) {
@@ -111,6 +209,29 @@ static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
     const u64 tiles = (q.m + 31) / 32;
     const int blocks = static_cast<int>(std::max<u64>(1, std::min<u64>((tiles + kRadiusWarps - 1) / kRadiusWarps,
                                                                       static_cast<u64>(ctx->sm_count) * 64)));
+    const FloatTest ft = make_float_test(r, std::max(c->bmax, q.bmax));
+    if (ft.enabled && q.f && t->tf && c->pf) {
+        u64* counter = dalloc_t<u64>(ctx, 1);
+        LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
+        const int pblocks = static_cast<int>(std::max<u64>(
+            1, std::min<u64>((tiles + kRadiusWarps - 1) / kRadiusWarps, static_cast<u64>(ctx->sm_count) * 8)));
+#define LO_RADIUS_F(S)                                                                          \
+    case S:                                                                                     \
+        radius_float_kernel<S, FILL><<<pblocks, kRadiusThreads, 0, ctx->stream>>>(             \
+            t->tf, c->pf, c->x, c->y, c->z, q, ft, r, r2, counts, offsets, out, counter);       \
+        break;
+        switch (shape) {
+            LO_RADIUS_F(LO_SPHERE)
+            LO_RADIUS_F(LO_CIRCLE)
+            LO_RADIUS_F(LO_CUBE)
+            LO_RADIUS_F(LO_SQUARE)
+            default: throw Error(LO_INVALID_ARGUMENT, "unknown kernel shape");
+        }
+#undef LO_RADIUS_F
+        LO_CHECK_LAUNCH();
+        dfree(ctx, counter);
+        return;
+    }
 #define LO_RADIUS_CASE(S)                                                                        \
     case S:                                                                                      \
         radius_kernel<S, FILL><<<blocks, kRadiusThreads, 0, ctx->stream>>>(t->tn, c->x, c->y,    \
@@ -192,23 +313,32 @@ u32* upload_centres(lo_context* ctx, const u32* centres_host, u64 m, u64 n) {
     return d;
 }
 
-// Explicit query points (AoS host) -> SoA device.
-void upload_points(lo_context* ctx, const double* xyz_host, u64 m, double** x, double** y,
-                   double** z) {
+// Explicit query points (AoS host) -> SoA device, plus their FP32 filter copies relative to
+// the cloud origin; *bmax bounds |query - origin| on every axis.
+void upload_points(lo_context* ctx, const lo_coded* c, const double* xyz_host, u64 m, double** x,
+                   double** y, double** z, float4** f, double* bmax) {
     std::vector<double> sx(m), sy(m), sz(m);
+    std::vector<float4> sf(m);
+    double b = 0.0;
     for (u64 i = 0; i < m; ++i) {
         sx[i] = xyz_host[3 * i];
         sy[i] = xyz_host[3 * i + 1];
         sz[i] = xyz_host[3 * i + 2];
         require(std::isfinite(sx[i]) && std::isfinite(sy[i]) && std::isfinite(sz[i]),
                 LO_INVALID_ARGUMENT, "kernel center must be finite");
+        const double rx = sx[i] - c->origin[0], ry = sy[i] - c->origin[1], rz = sz[i] - c->origin[2];
+        sf[i] = make_float4(static_cast<float>(rx), static_cast<float>(ry), static_cast<float>(rz), 0.f);
+        b = std::max({b, std::fabs(rx), std::fabs(ry), std::fabs(rz)});
     }
+    *bmax = b * (1.0 + 1e-12);
     *x = dalloc_t<double>(ctx, m);
     *y = dalloc_t<double>(ctx, m);
     *z = dalloc_t<double>(ctx, m);
+    *f = dalloc_t<float4>(ctx, m);
     LO_CUDA(cudaMemcpyAsync(*x, sx.data(), 8 * m, cudaMemcpyHostToDevice, ctx->stream));
     LO_CUDA(cudaMemcpyAsync(*y, sy.data(), 8 * m, cudaMemcpyHostToDevice, ctx->stream));
     LO_CUDA(cudaMemcpyAsync(*z, sz.data(), 8 * m, cudaMemcpyHostToDevice, ctx->stream));
+    LO_CUDA(cudaMemcpyAsync(*f, sf.data(), 16 * m, cudaMemcpyHostToDevice, ctx->stream));
     sync(ctx);
 }
 
@@ -228,8 +358,9 @@ int lo_radius(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int
                 LO_INVALID_ARGUMENT, "unknown radius method");
         require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
         const u64 rows = centres_host ? m : coded->n;
+        ensure_float_shadows(ctx, coded, tree);
         u32* cidx = upload_centres(ctx, centres_host, m, coded->n);
-        Queries q{coded->x, coded->y, coded->z, cidx, rows};
+        Queries q{coded->x, coded->y, coded->z, cidx, rows, coded->pf, coded->bmax};
         try {
             *out = radius_search(ctx, tree, coded, shape, radius, q, fingerprint != 0);
         } catch (...) {
@@ -243,16 +374,19 @@ int lo_radius(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int
 int lo_radius_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int shape,
                      double radius, const double* queries_host, uint64_t m, lo_csr** out) {
     return api([&] {
-        double *x = nullptr, *y = nullptr, *z = nullptr;
-        if (m) upload_points(ctx, queries_host, m, &x, &y, &z);
-        Queries q{x, y, z, nullptr, m};
+        require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
+        ensure_float_shadows(ctx, coded, tree);
+        double *x = nullptr, *y = nullptr, *z = nullptr, bmax = 0.0;
+        float4* f = nullptr;
+        if (m) upload_points(ctx, coded, queries_host, m, &x, &y, &z, &f, &bmax);
+        Queries q{x, y, z, nullptr, m, f, bmax};
         try {
             *out = radius_search(ctx, tree, coded, shape, radius, q, true);
         } catch (...) {
-            dfree(ctx, x), dfree(ctx, y), dfree(ctx, z);
+            dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f);
             throw;
         }
-        dfree(ctx, x), dfree(ctx, y), dfree(ctx, z);
+        dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f);
     });
 }
 
@@ -264,7 +398,9 @@ int lo_radius_range(lo_context* ctx, const lo_octree* tree, const lo_coded* code
                 LO_INVALID_ARGUMENT, "unknown radius method");
         require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
         require(begin <= end && end <= coded->n, LO_INVALID_ARGUMENT, "centre range out of bounds");
-        Queries q{coded->x + begin, coded->y + begin, coded->z + begin, nullptr, end - begin};
+        ensure_float_shadows(ctx, coded, tree);
+        Queries q{coded->x + begin, coded->y + begin, coded->z + begin, nullptr, end - begin,
+                  coded->pf + begin, coded->bmax};
         *out = radius_search(ctx, tree, coded, shape, radius, q, fingerprint != 0);
     });
 }

@@ -241,17 +241,48 @@ __global__ void __launch_bounds__(kSortThreads, 3) onesweep_pass(
 }
 
 // ---- K4: gather into SFC order, SoA f64 ---------------------------------------------------
+// Also writes the FP32 filter copy fl32(fl64(p - origin)) (search_common.cuh error bounds).
 __global__ void __launch_bounds__(256) gather_soa(const double* __restrict__ xyz,
                                                   const u32* __restrict__ perm, u64 n,
                                                   double* __restrict__ x, double* __restrict__ y,
-                                                  double* __restrict__ z) {
+                                                  double* __restrict__ z, float4* __restrict__ pf,
+                                                  double ox, double oy, double oz) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
          i += (u64)gridDim.x * blockDim.x) {
         const u64 o = perm[i];
-        x[i] = xyz[3 * o];
-        y[i] = xyz[3 * o + 1];
-        z[i] = xyz[3 * o + 2];
+        const double a = xyz[3 * o], b = xyz[3 * o + 1], c = xyz[3 * o + 2];
+        x[i] = a;
+        y[i] = b;
+        z[i] = c;
+        pf[i] = make_float4(__double2float_rn(a - ox), __double2float_rn(b - oy),
+                            __double2float_rn(c - oz), 0.f);
     }
+}
+
+__global__ void __launch_bounds__(256) float_points(const double* __restrict__ x,
+                                                    const double* __restrict__ y,
+                                                    const double* __restrict__ z, u64 n,
+                                                    float4* __restrict__ pf, double ox, double oy,
+                                                    double oz) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
+         i += (u64)gridDim.x * blockDim.x)
+        pf[i] = make_float4(__double2float_rn(x[i] - ox), __double2float_rn(y[i] - oy),
+                            __double2float_rn(z[i] - oz), 0.f);
+}
+
+void build_float_points(lo_context* ctx, lo_coded* c) {
+    if (c->pf) return;
+    c->pf = dalloc_t<float4>(ctx, c->n);
+    float_points<<<std::max<u64>(1, std::min<u64>((c->n + 255) / 256, ctx->sm_count * 8ull)), 256, 0,
+                   ctx->stream>>>(c->x, c->y, c->z, c->n, c->pf, c->origin[0], c->origin[1],
+                                  c->origin[2]);
+    LO_CHECK_LAUNCH();
+}
+
+static void set_origin(lo_coded* c) {
+    for (int a = 0; a < 3; ++a) c->origin[a] = c->disc_box[a];
+    c->bmax = std::max({c->disc_box[3] - c->disc_box[0], c->disc_box[4] - c->disc_box[1],
+                        c->disc_box[5] - c->disc_box[2]});
 }
 
 __global__ void iota_u32(u32* p, u64 n) {
@@ -481,7 +512,10 @@ static lo_coded* reorder_device(lo_context* ctx, const double* xyz, u64 n, int c
         c->x = dalloc_t<double>(ctx, n);
         c->y = dalloc_t<double>(ctx, n);
         c->z = dalloc_t<double>(ctx, n);
-        gather_soa<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(xyz, c->perm, n, c->x, c->y, c->z);
+        c->pf = dalloc_t<float4>(ctx, n);
+        set_origin(c);
+        gather_soa<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(
+            xyz, c->perm, n, c->x, c->y, c->z, c->pf, c->origin[0], c->origin[1], c->origin[2]);
         LO_CHECK_LAUNCH();
         stage_end(ctx);
         sync(ctx);
@@ -491,6 +525,7 @@ static lo_coded* reorder_device(lo_context* ctx, const double* xyz, u64 n, int c
         dfree(ctx, c->x);
         dfree(ctx, c->y);
         dfree(ctx, c->z);
+        dfree(ctx, c->pf);
         delete c;
         throw;
     }
@@ -652,6 +687,7 @@ int lo_coded_destroy(lo_coded* c) {
         dfree(ctx, c->z);
         dfree(ctx, c->codes);
         dfree(ctx, c->perm);
+        dfree(ctx, c->pf);
         delete c;
     });
 }
@@ -668,6 +704,7 @@ int lo_coded_create_empty(lo_context* ctx, const lo_coded_info* info, lo_coded**
         std::memcpy(c->disc_box, info->disc_box, sizeof c->disc_box);
         std::memcpy(c->cloud_box, info->cloud_box, sizeof c->cloud_box);
         std::memcpy(c->scale, info->scale, sizeof c->scale);
+        set_origin(c);  // pf is rebuilt lazily from the broadcast coordinates
         try {
             c->x = dalloc_t<double>(ctx, c->n);
             c->y = dalloc_t<double>(ctx, c->n);

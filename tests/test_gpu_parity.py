@@ -155,6 +155,41 @@ def test_grid_ties_offcloud_centres(ctx, oracle):
         assert np.array_equal(row, oracle.radius_brute(xs, c, 1.0, 0))
 
 
+@pytest.mark.parametrize("shape", [0, 1, 2, 3])
+def test_boundary_band_exact(ctx, oracle, shape):
+    """Points placed within a few ulps of the kernel boundary: the FP32 filter must hand
+    them to the exact FP64 predicate (strict '<' of geometry.hpp:127-140)."""
+    rng = np.random.default_rng(77 + shape)
+    centres = rng.uniform(200, 800, (64, 3))
+    r = 2.75
+    pts = [rng.uniform(0, 1000, (20000, 3))]
+    for c in centres:
+        d = rng.normal(size=(200, 3))
+        if shape in (1, 3):
+            d[:, 2] = 0.0
+        if shape in (0, 1):
+            d /= np.linalg.norm(d, axis=1, keepdims=True)
+        else:
+            d /= np.abs(d).max(axis=1, keepdims=True)
+        scale = r * (1.0 + rng.choice([-1, 0, 1], 200)[:, None] * rng.uniform(0, 4e-16, (200, 1)))
+        shell = c + d * scale
+        if shape in (1, 3):
+            shell[:, 2] = c[2] + rng.uniform(-5, 5, 200)
+        pts.append(shell)
+        pts.append(c[None, :])
+    pts = np.concatenate(pts)
+    coded, tree = pipeline(pts, 1, 32)
+    xs = coded.cloud.points
+    inv = lo.invert_permutation(coded.permutation)
+    base = 20000
+    qidx = [int(inv[base + i * 201 + 200]) for i in range(len(centres))]
+    res = lo.run_radius_batch(tree, coded, lo.RadiusMethod.Lin, lo.KernelShape(shape), r,
+                              lo.BatchOptions(collect_results=True))
+    for q in qidx:
+        want = oracle.radius_brute(xs, xs[q], r, shape)
+        assert np.array_equal(res.indices[res.offsets[q]:res.offsets[q + 1]], want)
+
+
 # ---- edge cases the reference tests -------------------------------------------------------
 def test_edge_cases(ctx, oracle):
     with pytest.raises(lo.InvalidArgument):
