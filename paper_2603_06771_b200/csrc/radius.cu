@@ -11,12 +11,12 @@
 #include <algorithm>
 #include <cmath>
 
-#include "search_common.cuh"
+#include <cstdlib>
+
+#include "radius_pt.cuh"
 
 namespace lo {
 
-constexpr int kRadiusWarps = 4;
-constexpr int kRadiusThreads = 32 * kRadiusWarps;
 
 template <int SHAPE, bool FILL>
 __global__ void __launch_bounds__(kRadiusThreads) radius_kernel(
@@ -86,104 +86,6 @@ __global__ void __launch_bounds__(kRadiusThreads) radius_kernel(
     }
 }
 
-// Same walk with the FP32 filter (search_common.cuh): node relations and point tests run in
-// FP32 with rigorous margins; only points inside the uncertainty band re-run the exact FP64
-// predicate, so the index sets are the reference's bit for bit.
-template <int SHAPE, bool FILL>
-__global__ void __launch_bounds__(kRadiusThreads, 8) radius_float_kernel(
-    const TNodeF* __restrict__ tf, const float4* __restrict__ pf, const double* __restrict__ px,
-    const double* __restrict__ py, const double* __restrict__ pz, Queries q, FloatTest ft,
-    double r, double r2, u32* __restrict__ counts, const u64* __restrict__ offsets,
-    u32* __restrict__ out, u64* tile_counter) {
-    __shared__ u32 stack_s[kRadiusWarps][kStackCap];
-    __shared__ float4 sp_s[kRadiusWarps][32];
-    __shared__ float4 sq_s[kRadiusWarps][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    u32* stack = stack_s[w];
-    float4* spts = sp_s[w];
-    float4* squeries = sq_s[w];
-    const u64 ntiles = (q.m + 31) / 32;
-    const int cl = lane & 7, grp = lane >> 3;
-    for (;;) {
-        // dynamic tile scheduling: heavy tiles (dense clusters) do not stall a static stride
-        u64 tile = 0;
-        if (lane == 0) tile = atomicAdd(reinterpret_cast<unsigned long long*>(tile_counter), 1ull);
-        tile = __shfl_sync(~0u, tile, 0);
-        if (tile >= ntiles) break;
-        const u64 qi = tile * 32 + lane;
-        const bool active = qi < q.m;
-        double cx = 0.0, cy = 0.0, cz = 0.0;
-        float4 qf = make_float4(INFINITY, INFINITY, INFINITY, 0.f);  // never near anything
-        if (active) {
-            load_query(q, qi, cx, cy, cz);
-            qf = load_query_f(q, qi);
-        }
-        __syncwarp();
-        squeries[lane] = qf;
-        u32 count = 0;
-        u32* row = nullptr;
-        if (FILL && active) row = out + offsets[qi];
-        int sp = 1;
-        if (lane == 0) stack[0] = 0;
-        __syncwarp();
-        while (sp > 0) {
-            const u32 t = stack[--sp];
-            const NodeF nd = load_node_f(tf, t);
-            if (nd.nchild != 0) {
-                // internal: lane (child cl, query group grp) tests child cl against the 8
-                // queries of its group; a child is kept when any of the 32 queries may reach it
-                bool keep = false;
-                if (cl < static_cast<int>(nd.nchild)) {
-                    const NodeF ch = load_node_f(tf, nd.child0 + cl);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) keep |= !disjoint_f<SHAPE>(squeries[8 * grp + j], ch, ft);
-                }
-                u32 s = __ballot_sync(~0u, keep);
-                s = (s | (s >> 8) | (s >> 16) | (s >> 24)) & 0xffu;
-                const int k = __popc(s);
-                __syncwarp();
-                if (lane < 8 && ((s >> lane) & 1u))
-                    stack[sp + k - 1 - __popc(s & ((1u << lane) - 1u))] = nd.child0 + lane;
-                sp += k;
-                __syncwarp();
-                continue;
-            }
-            int rel = kDisjoint;
-            if (active) rel = relation_f<SHAPE>(qf, nd, ft);
-            if (rel == kContains) {
-                if (FILL)
-                    for (u32 i = nd.begin; i < nd.end; ++i) row[count + (i - nd.begin)] = i;
-                count += nd.end - nd.begin;
-            }
-            if (!__ballot_sync(~0u, rel == kIntersects)) continue;
-            {
-                for (u32 base = nd.begin; base < nd.end; base += 32) {
-                    const u32 j = base + lane;
-                    __syncwarp();
-                    if (j < nd.end) spts[lane] = __ldg(pf + j);
-                    __syncwarp();
-                    if (rel == kIntersects) {
-                        const u32 cnt = min(32u, nd.end - base);
-                        for (u32 jj = 0; jj < cnt; ++jj) {
-                            int c = classify_f<SHAPE>(qf, spts[jj], ft);
-                            if (c == 2) {
-                                const u32 g = base + jj;
-                                c = contains<SHAPE>(cx, cy, cz, r, r2, px[g], py[g], pz[g]) ? 1 : 0;
-                            }
-                            if (c) {
-                                if (FILL) row[count] = base + jj;
-                                ++count;
-                            }
-                        }
-                    }
-                }
-            }
-        }
-        if (!FILL && active) counts[qi] = count;
-        __syncwarp();
-    }
-}
-
 // K8: FNV-1a-64 per row over its indices (search.cpp:345-347).
 __global__ void radius_digest(const u64* __restrict__ offsets, const u32* __restrict__ idx, u64 m,
                               u64* __restrict__ fps) {
@@ -211,14 +113,23 @@ static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
                                                                       static_cast<u64>(ctx->sm_count) * 64)));
     const FloatTest ft = make_float_test(r, std::max(c->bmax, q.bmax));
     if (ft.enabled && q.f && t->tf && c->pf) {
+        const float compact = static_cast<float>(4.0 * r);
         u64* counter = dalloc_t<u64>(ctx, 1);
         LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
         const int pblocks = static_cast<int>(std::max<u64>(
             1, std::min<u64>((tiles + kRadiusWarps - 1) / kRadiusWarps, static_cast<u64>(ctx->sm_count) * 8)));
+        // LO_RADIUS_LANE_QUERY=1 selects the lane = query variant (A/B comparisons)
+        static const bool lane_query = std::getenv("LO_RADIUS_LANE_QUERY") != nullptr;
 #define LO_RADIUS_F(S)                                                                          \
     case S:                                                                                     \
-        radius_float_kernel<S, FILL><<<pblocks, kRadiusThreads, 0, ctx->stream>>>(             \
-            t->tf, c->pf, c->x, c->y, c->z, q, ft, r, r2, counts, offsets, out, counter);       \
+        if (lane_query)                                                                         \
+            radius_float_kernel<S, FILL><<<pblocks, kRadiusThreads, 0, ctx->stream>>>(         \
+                t->tf, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, counts, offsets, out,    \
+                counter);                                                                       \
+        else                                                                                    \
+            radius_pt_kernel<S, FILL><<<pblocks, kPtThreads, 0, ctx->stream>>>(                \
+                t->tf, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, counts, offsets, out,    \
+                counter);                                                                       \
         break;
         switch (shape) {
             LO_RADIUS_F(LO_SPHERE)

@@ -1,0 +1,211 @@
+// radius_pt.cuh -- radius walk with lane = candidate point (K6 count / fill), used by radius.cu.
+//
+// Same traversal as radius_float.cuh (warp = 32 consecutive queries, child-parallel expansion
+// with per-group pruning), but leaves are not tested lane = query.  The points of every visited
+// leaf are appended, in code order, to a dense 32-slot shared-memory buffer; the buffer also
+// records which of the 32 queries reach any of its leaves.  A full buffer is processed with
+// lane j = buffer point j: for each interested query (two at a time, packed FP32 f32x2 math)
+// the warp ballots membership, so
+//   * no lane idles on small terrain leaves (~10 points) -- every slot is a real candidate,
+//   * the fill pass writes query L's members of the buffer with ONE coalesced store
+//     (position = row cursor + popc(mask below the lane)), no per-member loops,
+//   * rows stay ascending: buffers follow the DFS code order and slots keep point order.
+// Uncertainty-band points (search_common.cuh) are decided by the exact FP64 predicate.
+#pragma once
+
+#include "radius_float.cuh"
+
+namespace lo {
+
+constexpr int kPtWarps = 4;
+constexpr int kPtThreads = 32 * kPtWarps;
+
+struct PtShared {
+    u32 stack[kStackCap];
+    float4 buf[32];      // candidate (x, y, z) relative FP32, .w = point index bits
+    float4 qf[32];       // queries, FP32
+    double qd[32][3];    // queries, FP64 (band decisions)
+    u64 rows[32];        // fill: CSR cursor per query
+    u32 counts[32];      // count: members per query
+};
+
+// Decide band lanes exactly; returns the corrected membership ballot for query L.
+template <int SHAPE>
+__device__ __forceinline__ u32 band_fix(u32 in, u32 band, const PtShared& S, int L, int lane,
+                                        u32 idx, const double* __restrict__ px,
+                                        const double* __restrict__ py, const double* __restrict__ pz,
+                                        double r, double r2) {
+    bool m = false;
+    if ((band >> lane) & 1u)
+        m = contains<SHAPE>(S.qd[L][0], S.qd[L][1], S.qd[L][2], r, r2, px[idx], py[idx], pz[idx]);
+    return in | __ballot_sync(~0u, m);
+}
+
+template <int SHAPE, bool FILL>
+__device__ __forceinline__ void process_buffer(PtShared& S, u32 fill, u32 qmask, int lane,
+                                               const FloatTest& ft, float lo_thr, float hi_thr,
+                                               const double* __restrict__ px,
+                                               const double* __restrict__ py,
+                                               const double* __restrict__ pz, double r,
+                                               double r2, u32* __restrict__ out) {
+    constexpr bool kPacked = SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE;
+    const bool valid = static_cast<u32>(lane) < fill;
+    const float4 P = S.buf[lane];
+    const u32 idx = __float_as_uint(P.w);
+    const u64 PX = pack2(P.x, P.x), PY = pack2(P.y, P.y), PZ = pack2(P.z, P.z);
+    const u32 lt = (1u << lane) - 1u;
+    u32 rem = qmask;
+    while (rem) {
+        const int L0 = __ffs(rem) - 1;
+        rem &= rem - 1;
+        const bool two = rem != 0;
+        const int L1 = two ? __ffs(rem) - 1 : L0;
+        if (two) rem &= rem - 1;
+        const float4 q0 = S.qf[L0], q1 = S.qf[L1];
+        float v0, v1;
+        if (kPacked) {
+            const u64 dx = fsub2(PX, pack2(q0.x, q1.x));
+            const u64 dy = fsub2(PY, pack2(q0.y, q1.y));
+            u64 d2 = fmul2(dx, dx);
+            d2 = ffma2(dy, dy, d2);
+            if (SHAPE == LO_SPHERE) {
+                const u64 dz = fsub2(PZ, pack2(q0.z, q1.z));
+                d2 = ffma2(dz, dz, d2);
+            }
+            unpack2(d2, v0, v1);
+        } else {
+            v0 = metric_f<SHAPE>(q0, P);
+            v1 = metric_f<SHAPE>(q1, P);
+        }
+        u32 in0 = __ballot_sync(~0u, valid && v0 < lo_thr);
+        u32 in1 = __ballot_sync(~0u, valid && v1 < lo_thr);
+        const u32 b0 = __ballot_sync(~0u, valid && v0 < hi_thr) & ~in0;
+        const u32 b1 = __ballot_sync(~0u, valid && v1 < hi_thr) & ~in1;
+        if (b0 | b1) {  // rare: exact FP64 for the band points
+            if (b0) in0 = band_fix<SHAPE>(in0, b0, S, L0, lane, idx, px, py, pz, r, r2);
+            if (b1) in1 = band_fix<SHAPE>(in1, b1, S, L1, lane, idx, px, py, pz, r, r2);
+        }
+        if (!two) in1 = 0;
+        if (FILL) {
+            const u64 p0 = S.rows[L0];
+            const u64 p1 = S.rows[L1];
+            if ((in0 >> lane) & 1u) out[p0 + __popc(in0 & lt)] = idx;
+            if ((in1 >> lane) & 1u) out[p1 + __popc(in1 & lt)] = idx;
+            __syncwarp();
+            if (lane == 0) {
+                S.rows[L0] = p0 + __popc(in0);
+                if (two) S.rows[L1] = p1 + __popc(in1);
+            }
+        } else {
+            __syncwarp();
+            if (lane == 0) {
+                S.counts[L0] += __popc(in0);
+                if (two) S.counts[L1] += __popc(in1);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <int SHAPE, bool FILL>
+__global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
+    const TNodeF* __restrict__ tf, const float4* __restrict__ pf, const double* __restrict__ px,
+    const double* __restrict__ py, const double* __restrict__ pz, Queries q, FloatTest ft,
+    float compact, double r, double r2, u32* __restrict__ counts, const u64* __restrict__ offsets,
+    u32* __restrict__ out, u64* tile_counter) {
+    __shared__ PtShared shared_s[kPtWarps];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    PtShared& S = shared_s[w];
+    const u64 ntiles = (q.m + 31) / 32;
+    const int cl = lane & 7, grp = lane >> 3;
+    constexpr bool kSq = SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE;
+    const float lo_thr = kSq ? ft.t_lo : ft.r_lo;
+    const float hi_thr = kSq ? ft.t_hi : ft.r_hi;
+    for (;;) {
+        u64 tile = 0;
+        if (lane == 0) tile = atomicAdd(reinterpret_cast<unsigned long long*>(tile_counter), 1ull);
+        tile = __shfl_sync(~0u, tile, 0);
+        if (tile >= ntiles) break;
+        const u64 qi = tile * 32 + lane;
+        const bool active = qi < q.m;
+        double cx = 0.0, cy = 0.0, cz = 0.0;
+        float4 qf = make_float4(INFINITY, INFINITY, INFINITY, 0.f);  // never near anything
+        if (active) {
+            load_query(q, qi, cx, cy, cz);
+            qf = load_query_f(q, qi);
+        }
+        __syncwarp();
+        S.qf[lane] = qf;
+        S.qd[lane][0] = cx;
+        S.qd[lane][1] = cy;
+        S.qd[lane][2] = cz;
+        if (FILL) S.rows[lane] = active ? offsets[qi] : 0ull;
+        else S.counts[lane] = 0;
+        float gl[3] = {qf.x, qf.y, qf.z}, gh[3] = {qf.x, qf.y, qf.z};
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                gl[a] = fminf(gl[a], __shfl_xor_sync(~0u, gl[a], o));
+                gh[a] = fmaxf(gh[a], __shfl_xor_sync(~0u, gh[a], o));
+            }
+        }
+        const bool gcompact = fmaxf(fmaxf(gh[0] - gl[0], gh[1] - gl[1]), gh[2] - gl[2]) <= compact;
+        u32 fill = 0, qmask = 0;  // buffer occupancy and interested queries (warp-uniform)
+        int sp = 1;
+        if (lane == 0) S.stack[0] = 0;
+        __syncwarp();
+        while (sp > 0) {
+            const u32 t = S.stack[--sp];
+            const NodeF nd = load_node_f(tf, t);
+            if (nd.nchild != 0) {
+                bool keep = false;
+                if (cl < static_cast<int>(nd.nchild)) {
+                    const NodeF ch = load_node_f(tf, nd.child0 + cl);
+                    if (gcompact) {
+                        keep = !tile_disjoint_f<SHAPE>(gl, gh, ch, ft);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) keep |= !disjoint_f<SHAPE>(S.qf[8 * grp + j], ch, ft);
+                    }
+                }
+                u32 s = __ballot_sync(~0u, keep);
+                s = (s | (s >> 8) | (s >> 16) | (s >> 24)) & 0xffu;
+                const int k = __popc(s);
+                __syncwarp();
+                if (lane < 8 && ((s >> lane) & 1u))
+                    S.stack[sp + k - 1 - __popc(s & ((1u << lane) - 1u))] = nd.child0 + lane;
+                sp += k;
+                __syncwarp();
+                continue;
+            }
+            // leaf: which queries can reach it
+            const u32 want = __ballot_sync(~0u, active && !disjoint_f<SHAPE>(qf, nd, ft));
+            if (!want) continue;
+            for (u32 base = nd.begin; base < nd.end;) {
+                const u32 take = min(32u - fill, nd.end - base);
+                __syncwarp();
+                if (static_cast<u32>(lane) < take) {
+                    float4 p = __ldg(pf + base + lane);
+                    p.w = __uint_as_float(base + lane);
+                    S.buf[fill + lane] = p;
+                }
+                __syncwarp();
+                fill += take;
+                qmask |= want;
+                base += take;
+                if (fill == 32) {
+                    process_buffer<SHAPE, FILL>(S, fill, qmask, lane, ft, lo_thr, hi_thr, px, py, pz, r, r2, out);
+                    fill = 0;
+                    qmask = 0;
+                }
+            }
+        }
+        if (fill) process_buffer<SHAPE, FILL>(S, fill, qmask, lane, ft, lo_thr, hi_thr, px, py, pz, r, r2, out);
+        __syncwarp();
+        if (!FILL && active) counts[qi] = S.counts[lane];
+        __syncwarp();
+    }
+}
+
+}  // namespace lo

@@ -246,6 +246,20 @@ __device__ __forceinline__ bool disjoint_f(const float4& q, const NodeF& nd, con
     return fmaxf(nx, ny) >= ft.r_hi;
 }
 
+// FP32 metric compared against the FloatTest thresholds: squared distance (Sphere, Circle)
+// or L-inf distance (Cube, Square).
+template <int SHAPE>
+__device__ __forceinline__ float metric_f(const float4& q, const float4& p) {
+    const float dx = p.x - q.x, dy = p.y - q.y;
+    if (SHAPE == LO_SPHERE) {
+        const float dz = p.z - q.z;
+        return fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+    }
+    if (SHAPE == LO_CIRCLE) return fmaf(dy, dy, dx * dx);
+    if (SHAPE == LO_CUBE) return fmaxf(fmaxf(fabsf(dx), fabsf(dy)), fabsf(p.z - q.z));
+    return fmaxf(fabsf(dx), fabsf(dy));
+}
+
 // 1 = member, 0 = not a member, 2 = inside the uncertainty band (decide in FP64)
 template <int SHAPE>
 __device__ __forceinline__ int classify_f(const float4& q, const float4& p, const FloatTest& ft) {
