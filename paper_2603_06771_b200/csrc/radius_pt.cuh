@@ -24,9 +24,10 @@ struct PtShared {
     u32 stack[kStackCap];
     float4 buf[32];      // candidate (x, y, z) relative FP32, .w = point index bits
     float4 qf[32];       // queries, FP32
+    __align__(8) float qx[32];  // queries, FP32 SoA: (q[2p], q[2p+1]) loads as one f32x2
+    __align__(8) float qy[32];
+    __align__(8) float qz[32];
     double qd[32][3];    // queries, FP64 (band decisions)
-    u64 rows[32];        // fill: CSR cursor per query
-    u32 counts[32];      // count: members per query
 };
 
 // Decide band lanes exactly; returns the corrected membership ballot for query L.
@@ -41,69 +42,60 @@ __device__ __forceinline__ u32 band_fix(u32 in, u32 band, const PtShared& S, int
     return in | __ballot_sync(~0u, m);
 }
 
+// Tests the buffer's `fill` points (lane j = slot j) against the interested queries, taken as
+// fixed pairs (2p, 2p+1) so both query coordinates arrive as one packed f32x2 load.  Lane L
+// keeps query L's count (count pass) or its CSR cursor relative to the tile's first row
+// (fill pass) in a register.
 template <int SHAPE, bool FILL>
 __device__ __forceinline__ void process_buffer(PtShared& S, u32 fill, u32 qmask, int lane,
-                                               const FloatTest& ft, float lo_thr, float hi_thr,
+                                               float lo_thr, float hi_thr,
                                                const double* __restrict__ px,
                                                const double* __restrict__ py,
                                                const double* __restrict__ pz, double r,
-                                               double r2, u32* __restrict__ out) {
+                                               double r2, u32* __restrict__ out_tile, u32& mine) {
     constexpr bool kPacked = SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE;
-    const bool valid = static_cast<u32>(lane) < fill;
+    // slots >= fill hold +INF (staged that way), so they are never members; a query that is
+    // disjoint from every leaf of the buffer has d2_f >= near2_f >= t_hi for all its points,
+    // so testing it anyway yields an empty ballot -- no per-query interest masks are needed.
     const float4 P = S.buf[lane];
     const u32 idx = __float_as_uint(P.w);
     const u64 PX = pack2(P.x, P.x), PY = pack2(P.y, P.y), PZ = pack2(P.z, P.z);
     const u32 lt = (1u << lane) - 1u;
-    u32 rem = qmask;
-    while (rem) {
-        const int L0 = __ffs(rem) - 1;
-        rem &= rem - 1;
-        const bool two = rem != 0;
-        const int L1 = two ? __ffs(rem) - 1 : L0;
-        if (two) rem &= rem - 1;
-        const float4 q0 = S.qf[L0], q1 = S.qf[L1];
+    u32 pm = (qmask | (qmask >> 1)) & 0x55555555u;  // bit 2p: pair p has an interested query
+    while (pm) {
+        const int b = __ffs(pm) - 1;  // = 2p
+        pm &= pm - 1;
         float v0, v1;
         if (kPacked) {
-            const u64 dx = fsub2(PX, pack2(q0.x, q1.x));
-            const u64 dy = fsub2(PY, pack2(q0.y, q1.y));
+            const u64 dx = fsub2(PX, *reinterpret_cast<const u64*>(&S.qx[b]));
+            const u64 dy = fsub2(PY, *reinterpret_cast<const u64*>(&S.qy[b]));
             u64 d2 = fmul2(dx, dx);
             d2 = ffma2(dy, dy, d2);
             if (SHAPE == LO_SPHERE) {
-                const u64 dz = fsub2(PZ, pack2(q0.z, q1.z));
+                const u64 dz = fsub2(PZ, *reinterpret_cast<const u64*>(&S.qz[b]));
                 d2 = ffma2(dz, dz, d2);
             }
             unpack2(d2, v0, v1);
         } else {
-            v0 = metric_f<SHAPE>(q0, P);
-            v1 = metric_f<SHAPE>(q1, P);
+            v0 = metric_f<SHAPE>(S.qf[b], P);
+            v1 = metric_f<SHAPE>(S.qf[b + 1], P);
         }
-        u32 in0 = __ballot_sync(~0u, valid && v0 < lo_thr);
-        u32 in1 = __ballot_sync(~0u, valid && v1 < lo_thr);
-        const u32 b0 = __ballot_sync(~0u, valid && v0 < hi_thr) & ~in0;
-        const u32 b1 = __ballot_sync(~0u, valid && v1 < hi_thr) & ~in1;
-        if (b0 | b1) {  // rare: exact FP64 for the band points
-            if (b0) in0 = band_fix<SHAPE>(in0, b0, S, L0, lane, idx, px, py, pz, r, r2);
-            if (b1) in1 = band_fix<SHAPE>(in1, b1, S, L1, lane, idx, px, py, pz, r, r2);
+        u32 in0 = __ballot_sync(~0u, v0 < lo_thr);
+        u32 in1 = __ballot_sync(~0u, v1 < lo_thr);
+        const u32 h0 = __ballot_sync(~0u, v0 < hi_thr);
+        const u32 h1 = __ballot_sync(~0u, v1 < hi_thr);
+        if ((h0 ^ in0) | (h1 ^ in1)) {  // rare: band points, exact FP64 decides
+            if (h0 ^ in0) in0 = band_fix<SHAPE>(in0, h0 ^ in0, S, b, lane, idx, px, py, pz, r, r2);
+            if (h1 ^ in1) in1 = band_fix<SHAPE>(in1, h1 ^ in1, S, b + 1, lane, idx, px, py, pz, r, r2);
         }
-        if (!two) in1 = 0;
+        const u32 n0 = __popc(in0), n1 = __popc(in1);
         if (FILL) {
-            const u64 p0 = S.rows[L0];
-            const u64 p1 = S.rows[L1];
-            if ((in0 >> lane) & 1u) out[p0 + __popc(in0 & lt)] = idx;
-            if ((in1 >> lane) & 1u) out[p1 + __popc(in1 & lt)] = idx;
-            __syncwarp();
-            if (lane == 0) {
-                S.rows[L0] = p0 + __popc(in0);
-                if (two) S.rows[L1] = p1 + __popc(in1);
-            }
-        } else {
-            __syncwarp();
-            if (lane == 0) {
-                S.counts[L0] += __popc(in0);
-                if (two) S.counts[L1] += __popc(in1);
-            }
+            const u32 c0 = __shfl_sync(~0u, mine, b);
+            const u32 c1 = __shfl_sync(~0u, mine, b + 1);
+            if ((in0 >> lane) & 1u) out_tile[c0 + __popc(in0 & lt)] = idx;
+            if ((in1 >> lane) & 1u) out_tile[c1 + __popc(in1 & lt)] = idx;
         }
-        __syncwarp();
+        mine += lane == b ? n0 : (lane == b + 1 ? n1 : 0u);
     }
 }
 
@@ -136,11 +128,20 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
         }
         __syncwarp();
         S.qf[lane] = qf;
+        S.qx[lane] = qf.x;
+        S.qy[lane] = qf.y;
+        S.qz[lane] = qf.z;
         S.qd[lane][0] = cx;
         S.qd[lane][1] = cy;
         S.qd[lane][2] = cz;
-        if (FILL) S.rows[lane] = active ? offsets[qi] : 0ull;
-        else S.counts[lane] = 0;
+        // fill: rows of the tile are contiguous from offsets[tile*32]; cursors are relative
+        u32* out_tile = out;
+        u32 mine = 0;
+        if (FILL) {
+            const u64 tbase = offsets[tile * 32];
+            out_tile = out + tbase;
+            mine = active ? static_cast<u32>(offsets[qi] - tbase) : 0u;
+        }
         float gl[3] = {qf.x, qf.y, qf.z}, gh[3] = {qf.x, qf.y, qf.z};
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) {
@@ -190,20 +191,26 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
                     p.w = __uint_as_float(base + lane);
                     S.buf[fill + lane] = p;
                 }
-                __syncwarp();
                 fill += take;
                 qmask |= want;
                 base += take;
                 if (fill == 32) {
-                    process_buffer<SHAPE, FILL>(S, fill, qmask, lane, ft, lo_thr, hi_thr, px, py, pz, r, r2, out);
+                    __syncwarp();
+                    process_buffer<SHAPE, FILL>(S, fill, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2,
+                                                out_tile, mine);
                     fill = 0;
                     qmask = 0;
                 }
             }
         }
-        if (fill) process_buffer<SHAPE, FILL>(S, fill, qmask, lane, ft, lo_thr, hi_thr, px, py, pz, r, r2, out);
-        __syncwarp();
-        if (!FILL && active) counts[qi] = S.counts[lane];
+        if (fill) {
+            // partial last buffer: pad with never-member slots
+            if (static_cast<u32>(lane) >= fill) S.buf[lane] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+            __syncwarp();
+            process_buffer<SHAPE, FILL>(S, fill, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2, out_tile,
+                                        mine);
+        }
+        if (!FILL && active) counts[qi] = mine;
         __syncwarp();
     }
 }
