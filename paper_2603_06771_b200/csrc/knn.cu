@@ -74,6 +74,12 @@ struct LaneHeap {
 
 constexpr int kKnnSmemBudget = 200 * 1024;
 
+}  // namespace lo
+
+#include "knn_float.cuh"
+
+namespace lo {
+
 template <bool GLOBAL_HEAP>
 __global__ void __launch_bounds__(128) knn_kernel(const TNode* __restrict__ tn,
                                                   const double* __restrict__ px,
@@ -236,8 +242,10 @@ __global__ void locality_kernel(const u32* __restrict__ idx, u64 m, u32 keff,
     if (threadIdx.x < 33 && sb[threadIdx.x]) atomicAdd(&bins[threadIdx.x], sb[threadIdx.x]);
 }
 
+// seed_base >= 0: query i is cloud point seed_base + i (Full / range mode), which lets each
+// tile seed its heaps from the contiguous SFC window around it.
 static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_coded* c, u32 k,
-                                 const Queries& q, bool fingerprint) {
+                                 const Queries& q, bool fingerprint, i64 seed_base) {
     require(t != nullptr && c != nullptr, LO_INVALID_ARGUMENT, "null tree or cloud");
     require(k >= 1, LO_INVALID_ARGUMENT, "knn: k must be >= 1");
     auto* out = new lo_knn_result;
@@ -256,8 +264,11 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
         LO_CUDA(cudaEventRecord(e0, ctx->stream));
         out->idx = dalloc_t<u32>(ctx, q.m * kh);
         out->dist = dalloc_t<double>(ctx, q.m * kh);
+        const bool use_float = q.f && t->tf && c->pf;
         const size_t per_warp_heap = static_cast<size_t>(kh) * 32 * 12;
-        const size_t per_warp_fixed = sizeof(u32) * kStackCap + 96 * sizeof(double);
+        const size_t per_warp_fixed =
+            use_float ? sizeof(u32) * kStackCap + 4 * 32 + 16 * 32 + 16 * 16 + 8 * 16 + 4 * 32
+                      : sizeof(u32) * kStackCap + 96 * sizeof(double);
         const bool global_heap = per_warp_heap + per_warp_fixed > static_cast<size_t>(kKnnSmemBudget);
         int warps = 4;
         if (!global_heap)
@@ -270,7 +281,29 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
         const int blocks = static_cast<int>(std::max<u64>(
             1, std::min<u64>((tiles + warps - 1) / warps, static_cast<u64>(ctx->sm_count) * per_sm)));
         stage_begin(ctx, "knn");
-        if (q.m) {
+        if (q.m && use_float) {
+            const double E = std::ldexp(std::max(c->bmax, q.bmax), -23);
+            const u32 seed_half = std::max<u32>(16, kh);
+            u64* counter = dalloc_t<u64>(ctx, 1);
+            LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
+            if (global_heap) {
+                gd = dalloc_t<double>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
+                gi = dalloc_t<u32>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
+                LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                knn_float_kernel<true><<<blocks, 32 * warps, smem, ctx->stream>>>(
+                    t->tf, c->pf, c->x, c->y, c->z, c->n, q, seed_base, seed_half, E, kh, out->idx,
+                    out->dist, gd, gi, counter);
+            } else {
+                LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                knn_float_kernel<false><<<blocks, 32 * warps, smem, ctx->stream>>>(
+                    t->tf, c->pf, c->x, c->y, c->z, c->n, q, seed_base, seed_half, E, kh, out->idx,
+                    out->dist, nullptr, nullptr, counter);
+            }
+            LO_CHECK_LAUNCH();
+            dfree(ctx, counter);
+        } else if (q.m) {
             if (global_heap) {
                 gd = dalloc_t<double>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
                 gi = dalloc_t<u32>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
@@ -328,10 +361,11 @@ int lo_knn(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32
         require(k >= 1, LO_INVALID_ARGUMENT, "knn: k must be >= 1");
         require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
         const u64 rows = centres_host ? m : coded->n;
+        ensure_float_shadows(ctx, coded, tree);
         u32* cidx = upload_centres(ctx, centres_host, m, coded->n);
-        Queries q{coded->x, coded->y, coded->z, cidx, rows};
+        Queries q{coded->x, coded->y, coded->z, cidx, rows, coded->pf, coded->bmax};
         try {
-            *out = knn_search(ctx, tree, coded, k, q, fingerprint != 0);
+            *out = knn_search(ctx, tree, coded, k, q, fingerprint != 0, centres_host ? -1 : 0);
         } catch (...) {
             dfree(ctx, cidx);
             throw;
@@ -351,7 +385,7 @@ int lo_knn_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded,
         if (m) upload_points(ctx, coded, queries_host, m, &x, &y, &z, &f, &bmax);
         Queries q{x, y, z, nullptr, m, f, bmax};
         try {
-            *out = knn_search(ctx, tree, coded, k, q, true);
+            *out = knn_search(ctx, tree, coded, k, q, true, -1);
         } catch (...) {
             dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f);
             throw;
@@ -366,8 +400,10 @@ int lo_knn_range(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, 
         require(k >= 1, LO_INVALID_ARGUMENT, "knn: k must be >= 1");
         require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
         require(begin <= end && end <= coded->n, LO_INVALID_ARGUMENT, "centre range out of bounds");
-        Queries q{coded->x + begin, coded->y + begin, coded->z + begin, nullptr, end - begin};
-        *out = knn_search(ctx, tree, coded, k, q, fingerprint != 0);
+        ensure_float_shadows(ctx, coded, tree);
+        Queries q{coded->x + begin, coded->y + begin, coded->z + begin, nullptr, end - begin,
+                  coded->pf + begin, coded->bmax};
+        *out = knn_search(ctx, tree, coded, k, q, fingerprint != 0, static_cast<i64>(begin));
     });
 }
 

@@ -1,0 +1,268 @@
+// knn_float.cuh -- FP32-filtered exact kNN (K7), included by knn.cu.
+//
+// Exactness: the result is the first k points under (dist_sq, index) where dist_sq is the
+// reference's FP64 point_dist_sq (search.cpp:180-185).  Each lane (query) keeps an FP64 max-heap
+// of its k best; the FP32 copies only decide which candidates need the FP64 computation:
+// with w = the heap's current worst dist_sq, a candidate (or a node's lower bound) whose FP32
+// squared distance exceeds T(w) = w + M(w) provably has FP64 dist_sq > w, so it can neither
+// enter the heap nor tie with its top (M(w) is the same error bound as the radius filter,
+// evaluated at distance sqrt(w) with generous slack; search_common.cuh / DESIGN.md §4).
+//
+// Speed: for contiguous query ranges (Full mode) each tile first seeds its heaps from the
+// contiguous SFC window around its 32 points -- spatially the nearest points -- so T is tight
+// before the octree walk starts; the walk then enters a child only if some query's T reaches
+// it, and candidates already seen in the window are skipped by index.
+#pragma once
+
+#include "radius_float.cuh"
+
+namespace lo {
+
+struct KnnSmem {
+    u32* stack;
+    float* tq;      // per-query threshold T (FP32, +inf while the heap is not full)
+    float4* qf;     // per-query FP32 coordinates
+    float4* pa;     // staged candidate pairs (x0, x1, y0, y1)
+    float2* pb;     // (z0, z1)
+    u32* pidx;      // staged candidate indices
+};
+
+__device__ __forceinline__ float knn_threshold(double w, double E) {
+    const double u = 1.1920928955078125e-07;  // 2^-23
+    const double sw = sqrt(w);
+    const double dd = 2.0 * E + u * 2.0 * sw;
+    const double M = 1.5 * (12.0 * u * w + 4.0 * 1.7320508075688772 * sw * dd + 3.0 * dd * dd +
+                            4.0e-15 * w);
+    return __double2float_ru(w + M);
+}
+
+// One candidate j (global index g, FP32 squared distance v) for this lane.
+__device__ __forceinline__ void knn_offer(LaneHeap& heap, u32 k, double& worst_d, u32& worst_i,
+                                          float& T, double E, float v, u32 g, double cx, double cy,
+                                          double cz, const double* __restrict__ px,
+                                          const double* __restrict__ py,
+                                          const double* __restrict__ pz) {
+    if (v > T) return;
+    const double d = point_dist_sq(px[g], py[g], pz[g], cx, cy, cz);
+    if (heap.size < k) {
+        heap.push(d, g);
+        if (heap.size == k) {
+            worst_d = heap.hd[0];
+            worst_i = heap.hi[0];
+            T = knn_threshold(worst_d, E);
+        }
+    } else if (after(worst_d, worst_i, d, g)) {
+        heap.sift_down(d, g, k);
+        worst_d = heap.hd[0];
+        worst_i = heap.hi[0];
+        T = knn_threshold(worst_d, E);
+    }
+}
+
+// Tests the `cnt` staged candidates against this lane's query (pairs, packed FP32).
+__device__ __forceinline__ void knn_chunk(const KnnSmem& S, u32 cnt, bool active, u64 QX, u64 QY,
+                                          u64 QZ, LaneHeap& heap, u32 k, double& worst_d,
+                                          u32& worst_i, float& T, double E, double cx, double cy,
+                                          double cz, const double* __restrict__ px,
+                                          const double* __restrict__ py,
+                                          const double* __restrict__ pz, u32 skip_lo, u32 skip_hi) {
+    if (!active) return;
+    const u32 npairs = (cnt + 1) >> 1;
+    for (u32 pp = 0; pp < npairs; ++pp) {
+        const float4 a = S.pa[pp];
+        const float2 b = S.pb[pp];
+        const u64 dx = fsub2(pack2(a.x, a.y), QX);
+        const u64 dy = fsub2(pack2(a.z, a.w), QY);
+        const u64 dz = fsub2(pack2(b.x, b.y), QZ);
+        u64 d2 = fmul2(dx, dx);
+        d2 = ffma2(dy, dy, d2);
+        d2 = ffma2(dz, dz, d2);
+        float v0, v1;
+        unpack2(d2, v0, v1);
+        if (v0 <= T) {
+            const u32 g = S.pidx[2 * pp];
+            if (g < skip_lo || g >= skip_hi)
+                knn_offer(heap, k, worst_d, worst_i, T, E, v0, g, cx, cy, cz, px, py, pz);
+        }
+        if (2 * pp + 1 < cnt && v1 <= T) {
+            const u32 g = S.pidx[2 * pp + 1];
+            if (g < skip_lo || g >= skip_hi)
+                knn_offer(heap, k, worst_d, worst_i, T, E, v1, g, cx, cy, cz, px, py, pz);
+        }
+    }
+}
+
+// Stage points [base, base + cnt) (cnt <= 32) of the sorted cloud as FP32 pairs.
+__device__ __forceinline__ void knn_stage(const KnnSmem& S, const float4* __restrict__ pf, u32 base,
+                                          u32 cnt, int lane) {
+    __syncwarp();
+    if (static_cast<u32>(lane) < cnt) {
+        const float4 p = __ldg(pf + base + lane);
+        float* a = reinterpret_cast<float*>(S.pa);
+        float* b = reinterpret_cast<float*>(S.pb);
+        const int pp = lane >> 1, h = lane & 1;
+        a[4 * pp + h] = p.x;
+        a[4 * pp + 2 + h] = p.y;
+        b[2 * pp + h] = p.z;
+        S.pidx[lane] = base + lane;
+    }
+    __syncwarp();
+}
+
+constexpr int kKnnFloatStack = kStackCap;
+
+template <bool GLOBAL_HEAP>
+__global__ void __launch_bounds__(128) knn_float_kernel(
+    const TNodeF* __restrict__ tf, const float4* __restrict__ pf, const double* __restrict__ px,
+    const double* __restrict__ py, const double* __restrict__ pz, u64 npoints, Queries q,
+    i64 seed_base, u32 seed_half, double E, u32 k, u32* __restrict__ out_idx,
+    double* __restrict__ out_dist, double* __restrict__ gheap_d, u32* __restrict__ gheap_i,
+    u64* tile_counter) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warps = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // per-warp shared layout (fixed part): stack, tq[32], qf[32], pa[16], pb[16], pidx[32]
+    constexpr size_t kFixed = sizeof(u32) * kKnnFloatStack + 4 * 32 + 16 * 32 + 16 * 16 + 8 * 16 + 4 * 32;
+    unsigned char* mine = smem + w * kFixed;
+    KnnSmem S;
+    S.stack = reinterpret_cast<u32*>(mine);
+    S.tq = reinterpret_cast<float*>(mine + sizeof(u32) * kKnnFloatStack);
+    S.qf = reinterpret_cast<float4*>(mine + sizeof(u32) * kKnnFloatStack + 4 * 32);
+    S.pa = reinterpret_cast<float4*>(mine + sizeof(u32) * kKnnFloatStack + 4 * 32 + 16 * 32);
+    S.pb = reinterpret_cast<float2*>(mine + sizeof(u32) * kKnnFloatStack + 4 * 32 + 16 * 32 + 16 * 16);
+    S.pidx = reinterpret_cast<u32*>(mine + sizeof(u32) * kKnnFloatStack + 4 * 32 + 16 * 32 + 16 * 16 + 8 * 16);
+    double* hd;
+    u32* hi;
+    if (GLOBAL_HEAP) {
+        const u64 slot = static_cast<u64>(blockIdx.x) * warps + w;
+        hd = gheap_d + slot * k * 32 + lane;
+        hi = gheap_i + slot * k * 32 + lane;
+    } else {
+        double* heaps_d = reinterpret_cast<double*>(smem + warps * kFixed);
+        u32* heaps_i = reinterpret_cast<u32*>(heaps_d + static_cast<u64>(warps) * k * 32);
+        hd = heaps_d + static_cast<u64>(w) * k * 32 + lane;
+        hi = heaps_i + static_cast<u64>(w) * k * 32 + lane;
+    }
+    const u64 ntiles = (q.m + 31) / 32;
+    const int cl = lane & 7, grp = lane >> 3;
+    for (;;) {
+        u64 tile = 0;
+        if (lane == 0) tile = atomicAdd(reinterpret_cast<unsigned long long*>(tile_counter), 1ull);
+        tile = __shfl_sync(~0u, tile, 0);
+        if (tile >= ntiles) break;
+        const u64 qi = tile * 32 + lane;
+        const bool active = qi < q.m;
+        double cx = 0.0, cy = 0.0, cz = 0.0;
+        float4 qf = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+        if (active) {
+            load_query(q, qi, cx, cy, cz);
+            qf = load_query_f(q, qi);
+        }
+        const u64 QX = pack2(qf.x, qf.x), QY = pack2(qf.y, qf.y), QZ = pack2(qf.z, qf.z);
+        LaneHeap heap{hd, hi, 0};
+        double worst_d = 0.0;
+        u32 worst_i = 0;
+        float T = active ? INFINITY : -INFINITY;  // inactive lanes want nothing
+        __syncwarp();
+        S.qf[lane] = qf;
+
+        // 1) seed from the contiguous SFC window around the tile (Full / range mode)
+        u32 skip_lo = 0, skip_hi = 0;
+        if (seed_base >= 0) {
+            const i64 t0 = seed_base + static_cast<i64>(tile * 32);
+            const i64 t1 = seed_base + static_cast<i64>(min(q.m, tile * 32 + 32));
+            i64 lo = t0 - static_cast<i64>(seed_half);
+            if (lo < 0) lo = 0;
+            i64 hi_ = t1 + static_cast<i64>(seed_half);
+            if (hi_ > static_cast<i64>(npoints)) hi_ = static_cast<i64>(npoints);
+            skip_lo = static_cast<u32>(lo);
+            skip_hi = static_cast<u32>(hi_);
+            for (u32 b = skip_lo; b < skip_hi; b += 32) {
+                const u32 cnt = min(32u, skip_hi - b);
+                knn_stage(S, pf, b, cnt, lane);
+                knn_chunk(S, cnt, active, QX, QY, QZ, heap, k, worst_d, worst_i, T, E, cx, cy, cz,
+                          px, py, pz, 0u, 0u);
+            }
+        }
+
+        // 2) octree walk; a node is entered if some query's threshold reaches its box
+        int sp = 1;
+        if (lane == 0) S.stack[0] = 0;
+        __syncwarp();
+        while (sp > 0) {
+            __syncwarp();
+            S.tq[lane] = T;
+            __syncwarp();
+            const u32 t = S.stack[--sp];
+            const NodeF nd = load_node_f(tf, t);
+            if (nd.nchild != 0) {
+                bool keep = false;
+                if (cl < static_cast<int>(nd.nchild)) {
+                    const NodeF ch = load_node_f(tf, nd.child0 + cl);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const float4 qq = S.qf[8 * grp + j];
+                        const float nx = fmaxf(fmaxf(ch.lo[0] - qq.x, qq.x - ch.hi[0]), 0.f);
+                        const float ny = fmaxf(fmaxf(ch.lo[1] - qq.y, qq.y - ch.hi[1]), 0.f);
+                        const float nz = fmaxf(fmaxf(ch.lo[2] - qq.z, qq.z - ch.hi[2]), 0.f);
+                        keep |= fmaf(nz, nz, fmaf(ny, ny, nx * nx)) <= S.tq[8 * grp + j];
+                    }
+                }
+                u32 s = __ballot_sync(~0u, keep);
+                s = (s | (s >> 8) | (s >> 16) | (s >> 24)) & 0xffu;
+                const int kk = __popc(s);
+                __syncwarp();
+                if (lane < 8 && ((s >> lane) & 1u))
+                    S.stack[sp + kk - 1 - __popc(s & ((1u << lane) - 1u))] = nd.child0 + lane;
+                sp += kk;
+                continue;
+            }
+            // leaf: skip if no lane's threshold reaches it, or it lies inside the seed window
+            if (nd.begin >= skip_lo && nd.end <= skip_hi) continue;
+            bool want = false;
+            if (active) {
+                const float nx = fmaxf(fmaxf(nd.lo[0] - qf.x, qf.x - nd.hi[0]), 0.f);
+                const float ny = fmaxf(fmaxf(nd.lo[1] - qf.y, qf.y - nd.hi[1]), 0.f);
+                const float nz = fmaxf(fmaxf(nd.lo[2] - qf.z, qf.z - nd.hi[2]), 0.f);
+                want = fmaf(nz, nz, fmaf(ny, ny, nx * nx)) <= T;
+            }
+            if (!__any_sync(~0u, want)) continue;
+            for (u32 b = nd.begin; b < nd.end; b += 32) {
+                const u32 cnt = min(32u, nd.end - b);
+                knn_stage(S, pf, b, cnt, lane);
+                knn_chunk(S, cnt, want, QX, QY, QZ, heap, k, worst_d, worst_i, T, E, cx, cy, cz, px,
+                          py, pz, skip_lo, skip_hi);
+            }
+        }
+
+        // 3) heap sort in place -> ascending (dist_sq, index); coalesced row writes
+        if (active) {
+            const u32 n = heap.size;
+            for (u32 e = n; e > 1; --e) {
+                const double td = hd[0];
+                const u32 ti = hi[0];
+                const double ld = hd[(e - 1) * 32];
+                const u32 li = hi[(e - 1) * 32];
+                hd[(e - 1) * 32] = td;
+                hi[(e - 1) * 32] = ti;
+                heap.sift_down(ld, li, e - 1);
+            }
+        }
+        __syncwarp();
+        const u64 left = q.m - tile * 32;
+        const u32 nact = left < 32 ? static_cast<u32>(left) : 32u;
+        for (u32 L = 0; L < nact; ++L) {
+            u32* oi = out_idx + (tile * 32 + L) * k;
+            double* od = out_dist + (tile * 32 + L) * k;
+            const double* rhd = hd - lane + L;
+            const u32* rhi = hi - lane + L;
+            for (u32 e = lane; e < k; e += 32) {
+                oi[e] = rhi[e * 32];
+                od[e] = rhd[e * 32];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace lo
