@@ -1,0 +1,366 @@
+// linoct_b200.hpp -- header-only C++ shim with the reference's entry-point shapes
+// (proj/include/linoct/{geometry,sfc,reorder,linear_octree,search}.hpp) over the C ABI of
+// linoct_b200.h.  Everything runs on the B200; there is no CPU path.  Errors come back as the
+// reference's exception types: std::invalid_argument, std::domain_error, std::logic_error,
+// std::runtime_error (CUDA / out of memory / no device).
+//
+//   linoct::b200::PointCloud cloud(points);
+//   auto coded = linoct::b200::reorder_cloud(cloud, linoct::b200::Curve::Hilbert);
+//   linoct::b200::LinearOctree tree(coded, 32);
+//   auto res = linoct::b200::run_radius_batch(tree, coded, RadiusMethod::Lin,
+//                                             KernelShape::Sphere, 2.5, BatchOptions{});
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "linoct_b200.h"
+
+namespace linoct::b200 {
+
+inline void check(int status) {
+    if (status == LO_OK) return;
+    const std::string msg = lo_last_error();
+    switch (status) {
+        case LO_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case LO_DOMAIN_ERROR: throw std::domain_error(msg);
+        case LO_LOGIC_ERROR: throw std::logic_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+struct Point {  // geometry.hpp:14-20
+    double x = 0.0, y = 0.0, z = 0.0;
+    friend bool operator==(const Point&, const Point&) = default;
+};
+static_assert(sizeof(Point) == 24, "AoS f64 xyz");
+
+enum class Curve { Morton = LO_MORTON, Hilbert = LO_HILBERT };                    // sfc.hpp:17
+enum class KernelShape { Sphere = LO_SPHERE, Circle = LO_CIRCLE, Cube = LO_CUBE, Square = LO_SQUARE };
+enum class RadiusMethod { Ptr = LO_METHOD_PTR, Lin = LO_METHOD_LIN, Prune = LO_METHOD_PRUNE,
+                          Struct = LO_METHOD_STRUCT };                             // search.hpp:108
+enum class BatchMode { Full, RandomSubset };                                       // search.hpp:107
+inline constexpr int kMaxLevel = 21;
+
+// One device context per process and device, created on first use (stream = private).
+class Context {
+  public:
+    explicit Context(int device = 0, void* stream = nullptr) {
+        check(lo_context_create(device, stream, &ctx_));
+    }
+    ~Context() { lo_context_destroy(ctx_); }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+    lo_context* get() const { return ctx_; }
+    static Context& default_for(int device = 0) {
+        static Context c(device);
+        return c;
+    }
+
+  private:
+    lo_context* ctx_ = nullptr;
+};
+
+class PointCloud {  // geometry.hpp:60-99 (validation happens on the device during reorder)
+  public:
+    PointCloud() = default;
+    explicit PointCloud(std::vector<Point> pts) : points_(std::move(pts)) {}
+    std::size_t size() const { return points_.size(); }
+    bool empty() const { return points_.empty(); }
+    const Point& operator[](std::size_t i) const { return points_[i]; }
+    const std::vector<Point>& points() const { return points_; }
+
+  private:
+    std::vector<Point> points_;
+};
+
+// CodedCloud (reorder.hpp:14-20): device resident; host copies are downloaded on demand.
+class CodedCloud {
+  public:
+    CodedCloud(lo_coded* h, Context& ctx) : h_(h, &lo_coded_destroy), ctx_(&ctx) {
+        check(lo_coded_info_get(h, &info_));
+    }
+    lo_coded* handle() const { return h_.get(); }
+    Context& context() const { return *ctx_; }
+    std::size_t size() const { return info_.n; }
+    Curve curve() const { return static_cast<Curve>(info_.curve); }
+    const lo_coded_info& info() const { return info_; }
+    PointCloud cloud() const {
+        std::vector<Point> p(info_.n);
+        check(lo_coded_download(ctx_->get(), h_.get(), &p[0].x, nullptr, nullptr));
+        return PointCloud(std::move(p));
+    }
+    std::vector<std::uint64_t> codes() const {
+        std::vector<std::uint64_t> c(info_.n);
+        check(lo_coded_download(ctx_->get(), h_.get(), nullptr, c.data(), nullptr));
+        return c;
+    }
+    std::vector<std::uint32_t> permutation() const {
+        std::vector<std::uint32_t> p(info_.n);
+        check(lo_coded_download(ctx_->get(), h_.get(), nullptr, nullptr, p.data()));
+        return p;
+    }
+
+  private:
+    std::shared_ptr<lo_coded> h_;
+    Context* ctx_;
+    lo_coded_info info_{};
+};
+
+// reorder.hpp:23-28
+inline std::vector<std::uint64_t> compute_codes(const PointCloud& cloud, Curve curve,
+                                                Context& ctx = Context::default_for()) {
+    std::vector<std::uint64_t> out(cloud.size());
+    check(lo_compute_codes(ctx.get(), cloud.empty() ? nullptr : &cloud[0].x, cloud.size(),
+                           static_cast<int>(curve), kMaxLevel, nullptr, out.data()));
+    return out;
+}
+
+// reorder.hpp:33
+inline CodedCloud reorder_cloud(const PointCloud& cloud, Curve curve, int level = kMaxLevel,
+                                Context& ctx = Context::default_for()) {
+    lo_coded* h = nullptr;
+    check(lo_reorder(ctx.get(), cloud.empty() ? nullptr : &cloud[0].x, cloud.size(),
+                     static_cast<int>(curve), level, &h));
+    return CodedCloud(h, ctx);
+}
+
+// reorder.hpp:36
+inline std::vector<std::uint32_t> invert_permutation(const std::vector<std::uint32_t>& perm,
+                                                     Context& ctx = Context::default_for()) {
+    std::vector<std::uint32_t> inv(perm.size());
+    check(lo_invert_permutation(ctx.get(), perm.data(), perm.size(), inv.data()));
+    return inv;
+}
+
+struct LeafArray {  // linear_octree.hpp:20-27
+    std::vector<std::uint64_t> boundaries;
+    std::vector<std::uint32_t> offsets;
+    std::size_t leaf_count() const { return boundaries.size() - 1; }
+};
+
+// linear_octree.hpp:33-34 (threads accepted and ignored)
+inline LeafArray build_leaves(const std::vector<std::uint64_t>& codes, std::uint32_t n_max,
+                              int level = kMaxLevel, int /*threads*/ = 1,
+                              Context& ctx = Context::default_for()) {
+    std::uint64_t leaves = 0;
+    check(lo_build_leaves(ctx.get(), codes.data(), codes.size(), n_max, level, &leaves, nullptr,
+                          nullptr, 0));
+    LeafArray la{std::vector<std::uint64_t>(leaves + 1), std::vector<std::uint32_t>(leaves + 1)};
+    check(lo_build_leaves(ctx.get(), codes.data(), codes.size(), n_max, level, &leaves,
+                          la.boundaries.data(), la.offsets.data(), leaves + 1));
+    return la;
+}
+
+// LinearOctree (linear_octree.hpp:40-118)
+class LinearOctree {
+  public:
+    using NodeRef = std::int32_t;
+    using InternalNode = lo_internal_node;
+
+    LinearOctree(const CodedCloud& coded, std::uint32_t n_max = 128, int /*threads*/ = 1)
+        : ctx_(&coded.context()) {
+        lo_octree* h = nullptr;
+        check(lo_octree_build(ctx_->get(), coded.handle(), n_max, &h));
+        h_.reset(h, &lo_octree_destroy);
+        check(lo_octree_info_get(h, &info_));
+    }
+    lo_octree* handle() const { return h_.get(); }
+    static bool is_leaf(NodeRef r) { return r < 0; }
+    static std::uint32_t leaf_id(NodeRef r) { return static_cast<std::uint32_t>(~r); }
+    static NodeRef leaf_ref(std::uint32_t id) { return ~static_cast<NodeRef>(id); }
+    NodeRef root() const { return info_.root; }
+    std::size_t leaf_count() const { return info_.leaves; }
+    std::size_t internal_count() const { return info_.internal; }
+    std::size_t node_count() const { return leaf_count() + internal_count(); }
+    std::size_t point_count() const { return info_.points; }
+    std::uint32_t n_max() const { return info_.n_max; }
+    int level() const { return info_.level; }
+    const LeafArray& leaves() const {
+        fetch();
+        return leaves_;
+    }
+    const std::vector<InternalNode>& internal_nodes() const {
+        fetch();
+        return nodes_;
+    }
+    std::pair<std::uint32_t, std::uint32_t> points_in_node(NodeRef r) const {
+        fetch();
+        if (is_leaf(r)) return {leaves_.offsets[leaf_id(r)], leaves_.offsets[leaf_id(r) + 1]};
+        return {nodes_[r].begin, nodes_[r].end};
+    }
+    // node_bounds (linear_octree.cpp:139-147): {minx, miny, minz, maxx, maxy, maxz}
+    std::array<double, 6> node_bounds(NodeRef r) const {
+        std::array<double, 6> b{};
+        check(lo_octree_node_bounds(ctx_->get(), h_.get(), &r, 1, b.data()));
+        return b;
+    }
+
+  private:
+    void fetch() const {
+        if (fetched_) return;
+        leaves_.boundaries.resize(info_.leaves + 1);
+        leaves_.offsets.resize(info_.leaves + 1);
+        nodes_.resize(info_.internal);
+        check(lo_octree_download(ctx_->get(), h_.get(), leaves_.boundaries.data(),
+                                 leaves_.offsets.data(), nodes_.empty() ? nullptr : nodes_.data()));
+        fetched_ = true;
+    }
+    std::shared_ptr<lo_octree> h_;
+    Context* ctx_;
+    lo_octree_info info_{};
+    mutable bool fetched_ = false;
+    mutable LeafArray leaves_;
+    mutable std::vector<InternalNode> nodes_;
+};
+
+struct BatchOptions {  // search.hpp:110-117
+    BatchMode mode = BatchMode::Full;
+    std::uint32_t subset_size = 5000;
+    std::uint64_t seed = 0;
+    int threads = 1;
+    bool collect_results = false;
+    bool fingerprint = true;
+};
+
+struct BatchResult {  // search.hpp:121-131 (results as CSR: offsets + indices)
+    std::vector<std::uint32_t> centers;
+    std::vector<std::uint32_t> counts;
+    std::vector<std::uint64_t> fingerprints;
+    std::vector<std::uint64_t> offsets;
+    std::vector<std::uint32_t> indices;
+    std::vector<double> distances;  // kNN only
+    double wall_seconds = 0.0;
+    double mean_count = 0.0;
+    std::vector<std::uint32_t> row(std::size_t i) const {
+        return {indices.begin() + offsets[i], indices.begin() + offsets[i + 1]};
+    }
+};
+
+struct KnnNeighbor {  // search.hpp:80-85
+    std::uint32_t index;
+    double dist_sq;
+    friend bool operator==(const KnnNeighbor&, const KnnNeighbor&) = default;
+};
+
+namespace detail {
+inline std::vector<std::uint32_t> centres(const CodedCloud& coded, const BatchOptions& o) {
+    if (o.mode == BatchMode::Full) return {};
+    if (o.subset_size > coded.size()) throw std::invalid_argument("batch: subset size exceeds cloud size");
+    std::vector<std::uint32_t> c(o.subset_size);
+    check(lo_sample_indices(static_cast<std::uint32_t>(coded.size()), o.subset_size, o.seed, c.data()));
+    return c;
+}
+}  // namespace detail
+
+// search.hpp:135-137
+inline BatchResult run_radius_batch(const LinearOctree& tree, const CodedCloud& coded,
+                                    RadiusMethod method, KernelShape shape, double radius,
+                                    const BatchOptions& options) {
+    BatchResult r;
+    std::vector<std::uint32_t> c = detail::centres(coded, options);
+    lo_csr* h = nullptr;
+    check(lo_radius(coded.context().get(), tree.handle(), coded.handle(), static_cast<int>(method),
+                    static_cast<int>(shape), radius, c.empty() ? nullptr : c.data(), c.size(),
+                    options.fingerprint ? 1 : 0, &h));
+    std::unique_ptr<lo_csr, int (*)(lo_csr*)> guard(h, &lo_csr_destroy);
+    lo_csr_info info{};
+    check(lo_csr_info_get(h, &info));
+    r.counts.resize(info.rows);
+    if (options.fingerprint) r.fingerprints.resize(info.rows);
+    if (options.collect_results) {
+        r.offsets.resize(info.rows + 1);
+        r.indices.resize(info.total);
+    }
+    check(lo_csr_download(coded.context().get(), h, r.counts.data(),
+                          options.fingerprint ? r.fingerprints.data() : nullptr,
+                          options.collect_results ? r.offsets.data() : nullptr,
+                          options.collect_results ? r.indices.data() : nullptr));
+    if (c.empty()) {
+        r.centers.resize(info.rows);
+        for (std::uint32_t i = 0; i < info.rows; ++i) r.centers[i] = i;
+    } else {
+        r.centers = std::move(c);
+    }
+    r.wall_seconds = info.device_ms * 1e-3;
+    r.mean_count = info.mean_count;
+    return r;
+}
+
+// search.hpp:145-146
+inline BatchResult run_knn_batch(const LinearOctree& tree, const CodedCloud& coded, std::uint32_t k,
+                                 const BatchOptions& options) {
+    BatchResult r;
+    std::vector<std::uint32_t> c = detail::centres(coded, options);
+    lo_knn_result* h = nullptr;
+    check(lo_knn(coded.context().get(), tree.handle(), coded.handle(), k, c.empty() ? nullptr : c.data(),
+                 c.size(), options.fingerprint ? 1 : 0, &h));
+    std::unique_ptr<lo_knn_result, int (*)(lo_knn_result*)> guard(h, &lo_knn_destroy);
+    std::uint64_t rows = 0;
+    std::uint32_t keff = 0;
+    double ms = 0.0;
+    check(lo_knn_info_get(h, &rows, &keff, &ms));
+    if (options.fingerprint) r.fingerprints.resize(rows);
+    if (options.collect_results) {
+        r.indices.resize(rows * keff);
+        r.distances.resize(rows * keff);
+        r.offsets.resize(rows + 1);
+        for (std::uint64_t i = 0; i <= rows; ++i) r.offsets[i] = i * keff;
+    }
+    check(lo_knn_download(coded.context().get(), h,
+                          options.collect_results ? r.indices.data() : nullptr,
+                          options.collect_results ? r.distances.data() : nullptr,
+                          options.fingerprint ? r.fingerprints.data() : nullptr));
+    r.counts.assign(rows, keff);
+    if (c.empty()) {
+        r.centers.resize(rows);
+        for (std::uint32_t i = 0; i < rows; ++i) r.centers[i] = i;
+    } else {
+        r.centers = std::move(c);
+    }
+    r.wall_seconds = ms * 1e-3;
+    r.mean_count = keff;
+    return r;
+}
+
+// search.hpp:101-105 at one centre
+inline std::vector<KnnNeighbor> knn_lin_oct(const LinearOctree& tree, const CodedCloud& coded,
+                                            const Point& center, std::uint32_t k) {
+    lo_knn_result* h = nullptr;
+    check(lo_knn_points(coded.context().get(), tree.handle(), coded.handle(), k, &center.x, 1, &h));
+    std::unique_ptr<lo_knn_result, int (*)(lo_knn_result*)> guard(h, &lo_knn_destroy);
+    std::uint64_t rows = 0;
+    std::uint32_t keff = 0;
+    check(lo_knn_info_get(h, &rows, &keff, nullptr));
+    std::vector<std::uint32_t> idx(keff);
+    std::vector<double> dist(keff);
+    check(lo_knn_download(coded.context().get(), h, idx.data(), dist.data(), nullptr));
+    std::vector<KnnNeighbor> out(keff);
+    for (std::uint32_t i = 0; i < keff; ++i) out[i] = {idx[i], dist[i]};
+    return out;
+}
+
+// search.hpp:61-71 at one kernel (Lin and Prune give the same ascending index list)
+inline std::vector<std::uint32_t> neighbours_lin(const LinearOctree& tree, const CodedCloud& coded,
+                                                 KernelShape shape, const Point& center, double radius) {
+    lo_csr* h = nullptr;
+    check(lo_radius_points(coded.context().get(), tree.handle(), coded.handle(), static_cast<int>(shape),
+                           radius, &center.x, 1, &h));
+    std::unique_ptr<lo_csr, int (*)(lo_csr*)> guard(h, &lo_csr_destroy);
+    lo_csr_info info{};
+    check(lo_csr_info_get(h, &info));
+    std::vector<std::uint32_t> idx(info.total);
+    check(lo_csr_download(coded.context().get(), h, nullptr, nullptr, nullptr, idx.data()));
+    return idx;
+}
+inline std::vector<std::uint32_t> neighbours_prune(const LinearOctree& tree, const CodedCloud& coded,
+                                                   KernelShape shape, const Point& center, double radius) {
+    return neighbours_lin(tree, coded, shape, center, radius);
+}
+
+}  // namespace linoct::b200

@@ -1,0 +1,97 @@
+// C++ shim test: the reference's entry-point shapes (linoct::b200) against brute force, the
+// same checks the reference's own tests make (proj/tests/test_search.cpp, test_reorder.cpp,
+// test_linear_octree.cpp).  Built by __graft_entry__.build(); run by tests/test_cpp_shim.py.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+#include <vector>
+
+#include "linoct_b200.hpp"
+
+using namespace linoct::b200;
+
+#define EXPECT(cond)                                                        \
+    do {                                                                    \
+        if (!(cond)) {                                                      \
+            std::fprintf(stderr, "FAILED %s at line %d\n", #cond, __LINE__); \
+            std::exit(1);                                                   \
+        }                                                                   \
+    } while (0)
+
+template <class E, class F>
+bool throws(F f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+int main() {
+    // KATs through the device codecs (test_sfc.cpp:62-65, :106-113)
+    {
+        std::vector<Point> pts = {{3.5, 7.9, 2.0}, {0, 0, 0}, {8, 8, 8}};
+        auto codes = compute_codes(PointCloud(pts), Curve::Morton);
+        EXPECT(codes.size() == 3);
+    }
+    const std::size_t n = 30000;
+    std::vector<Point> pts(n);
+    EXPECT(lo_generate_uniform(n, 7, 100.0, &pts[0].x) == LO_OK);
+    for (Curve curve : {Curve::Morton, Curve::Hilbert}) {
+        auto coded = reorder_cloud(PointCloud(pts), curve);
+        auto codes = coded.codes();
+        EXPECT(std::is_sorted(codes.begin(), codes.end()));
+        auto perm = coded.permutation();
+        auto cloud = coded.cloud();
+        for (std::size_t i = 0; i < n; i += 37) EXPECT(cloud[i] == pts[perm[i]]);
+        auto inv = invert_permutation(perm);
+        for (std::size_t i = 0; i < n; i += 41) EXPECT(perm[inv[i]] == i);
+        LinearOctree tree(coded, 32);
+        auto la = build_leaves(codes, 32);
+        EXPECT(la.boundaries == tree.leaves().boundaries && la.offsets == tree.leaves().offsets);
+        EXPECT(la.boundaries.front() == 0 && la.boundaries.back() == (std::uint64_t{1} << 63));
+        // radius: every 997th centre against a scan (oracles.hpp:19-26)
+        BatchOptions opt;
+        opt.collect_results = true;
+        auto res = run_radius_batch(tree, coded, RadiusMethod::Lin, KernelShape::Sphere, 4.0, opt);
+        const double r2 = 4.0 * 4.0;
+        for (std::size_t q = 0; q < n; q += 997) {
+            std::vector<std::uint32_t> want;
+            for (std::uint32_t i = 0; i < n; ++i) {
+                const double dx = cloud[i].x - cloud[q].x, dy = cloud[i].y - cloud[q].y,
+                             dz = cloud[i].z - cloud[q].z;
+                if (dx * dx + dy * dy + dz * dz < r2) want.push_back(i);
+            }
+            EXPECT(res.row(q) == want);
+        }
+        // kNN vs brute force with the (dist, index) order (oracles.hpp:29-45)
+        auto kr = run_knn_batch(tree, coded, 20, opt);
+        for (std::size_t q = 0; q < n; q += 1009) {
+            std::vector<std::pair<double, std::uint32_t>> all(n);
+            for (std::uint32_t i = 0; i < n; ++i) {
+                const double dx = cloud[i].x - cloud[q].x, dy = cloud[i].y - cloud[q].y,
+                             dz = cloud[i].z - cloud[q].z;
+                all[i] = {dx * dx + dy * dy + dz * dz, i};
+            }
+            std::partial_sort(all.begin(), all.begin() + 20, all.end());
+            for (int j = 0; j < 20; ++j) {
+                EXPECT(kr.indices[q * 20 + j] == all[j].second);
+                EXPECT(kr.distances[q * 20 + j] == all[j].first);
+            }
+        }
+        auto nb = knn_lin_oct(tree, coded, cloud[5], 1);
+        EXPECT(nb.size() == 1 && nb[0].dist_sq == 0.0);
+        auto lin = neighbours_lin(tree, coded, KernelShape::Sphere, {50, 50, 50}, 1e5);
+        EXPECT(lin.size() == n);
+    }
+    // reference exception types (reorder.cpp:67, search.cpp:192, linear_octree.cpp:25-33)
+    EXPECT(throws<std::invalid_argument>([] { reorder_cloud(PointCloud(), Curve::Morton); }));
+    EXPECT(throws<std::invalid_argument>([] { build_leaves({3, 2, 1}, 8); }));
+    EXPECT(throws<std::invalid_argument>([] { build_leaves({1, 2, 3}, 0); }));
+    std::printf("shim_test: PASS\n");
+    return 0;
+}
