@@ -47,6 +47,25 @@ void dfree(lo_context* ctx, void* p) {
 
 void sync(lo_context* ctx) { LO_CUDA(cudaStreamSynchronize(ctx->stream)); }
 
+void* arena(lo_context* ctx, size_t bytes) {
+    if (ctx->arena_bytes >= bytes) return ctx->arena;
+    if (ctx->arena) {
+        sync(ctx);
+        cudaFree(ctx->arena);
+        ctx->arena = nullptr;
+        ctx->arena_bytes = 0;
+    }
+    const size_t want = bytes + bytes / 4;  // headroom: a slightly larger batch reuses it
+    cudaError_t e = cudaMalloc(&ctx->arena, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        ctx->arena = nullptr;
+        throw Error(LO_OUT_OF_MEMORY, "scratch arena allocation failed");
+    }
+    ctx->arena_bytes = want;
+    return ctx->arena;
+}
+
 void stage_begin(lo_context* ctx, const char* name) {
     if (!ctx->timing) return;
     lo_context::Stage s{name, nullptr, nullptr};
@@ -357,6 +376,7 @@ int lo_context_destroy(lo_context* ctx) {
             cudaEventDestroy(s.b);
         }
         if (ctx->pinned_scratch) cudaFreeHost(ctx->pinned_scratch);
+        if (ctx->arena) cudaFree(ctx->arena);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
         delete ctx;
     });

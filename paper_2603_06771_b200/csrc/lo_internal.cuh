@@ -98,6 +98,8 @@ struct lo_context {
     std::vector<Stage> stages;          // pending stage events (resolved on query)
     std::vector<std::pair<std::string, float>> stage_ms;
     void* pinned_scratch = nullptr;     // small pinned buffer for scalar D2H
+    void* arena = nullptr;              // persistent device scratch (radius records)
+    size_t arena_bytes = 0;
 };
 
 struct lo_coded {
@@ -167,6 +169,9 @@ template <class T>
 T* dalloc_t(lo_context* ctx, size_t count) {
     return static_cast<T*>(dalloc(ctx, count * sizeof(T) + (count == 0)));
 }
+// Persistent per-context scratch of at least `bytes` (grown on demand, reused across calls,
+// released with the context).  Throws LO_OUT_OF_MEMORY when it cannot grow.
+void* arena(lo_context* ctx, size_t bytes);
 void stage_begin(lo_context* ctx, const char* name);
 void stage_end(lo_context* ctx);
 void sync(lo_context* ctx);

@@ -10,7 +10,7 @@
 // reference's.
 #include <algorithm>
 #include <cmath>
-
+#include <cstdio>
 #include <cstdlib>
 
 #include "radius_pt.cuh"
@@ -104,32 +104,38 @@ __global__ void counts_from_offsets(const u64* __restrict__ offsets, u64 m, u32*
         counts[r] = static_cast<u32>(offsets[r + 1] - offsets[r]);
 }
 
+struct RecArgs {  // count-pass records for the replay fill (radius_pt.cuh)
+    u32* rec = nullptr;
+    u32 cap = 0;
+    u32* rec_n = nullptr;
+    const u32* list = nullptr;  // fill fallback: only these tiles
+    u64 list_n = 0;
+};
+
+static bool float_path(const lo_octree* t, const lo_coded* c, const Queries& q, double r) {
+    return make_float_test(r, std::max(c->bmax, q.bmax)).enabled && q.f && t->tf && c->pf;
+}
+
 template <bool FILL>
 static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const lo_coded* c,
-                          const Queries& q, double r, u32* counts, const u64* offsets, u32* out) {
+                          const Queries& q, double r, u32* counts, const u64* offsets, u32* out,
+                          const RecArgs& ra = RecArgs{}) {
     const double r2 = r * r;  // SearchKernel ctor (geometry.hpp:107)
-    const u64 tiles = (q.m + 31) / 32;
+    const u64 tiles = ra.list ? ra.list_n : (q.m + 31) / 32;
     const int blocks = static_cast<int>(std::max<u64>(1, std::min<u64>((tiles + kRadiusWarps - 1) / kRadiusWarps,
                                                                       static_cast<u64>(ctx->sm_count) * 64)));
-    const FloatTest ft = make_float_test(r, std::max(c->bmax, q.bmax));
-    if (ft.enabled && q.f && t->tf && c->pf) {
+    if (float_path(t, c, q, r)) {
+        const FloatTest ft = make_float_test(r, std::max(c->bmax, q.bmax));
         const float compact = static_cast<float>(4.0 * r);
         u64* counter = dalloc_t<u64>(ctx, 1);
         LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
         const int pblocks = static_cast<int>(std::max<u64>(
-            1, std::min<u64>((tiles + kRadiusWarps - 1) / kRadiusWarps, static_cast<u64>(ctx->sm_count) * 8)));
-        // LO_RADIUS_LANE_QUERY=1 selects the lane = query variant (A/B comparisons)
-        static const bool lane_query = std::getenv("LO_RADIUS_LANE_QUERY") != nullptr;
+            1, std::min<u64>((tiles + kPtWarps - 1) / kPtWarps, static_cast<u64>(ctx->sm_count) * 8)));
 #define LO_RADIUS_F(S)                                                                          \
     case S:                                                                                     \
-        if (lane_query)                                                                         \
-            radius_float_kernel<S, FILL><<<pblocks, kRadiusThreads, 0, ctx->stream>>>(         \
-                t->tf, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, counts, offsets, out,    \
-                counter);                                                                       \
-        else                                                                                    \
-            radius_pt_kernel<S, FILL><<<pblocks, kPtThreads, 0, ctx->stream>>>(                \
-                t->tf, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, counts, offsets, out,    \
-                counter);                                                                       \
+        radius_pt_kernel<S, FILL><<<pblocks, kPtThreads, 0, ctx->stream>>>(                    \
+            t->tf, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, counts, offsets, out,        \
+            counter, ra.rec, ra.cap, ra.rec_n, ra.list, ra.list_n);                             \
         break;
         switch (shape) {
             LO_RADIUS_F(LO_SPHERE)
@@ -143,6 +149,7 @@ static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
         dfree(ctx, counter);
         return;
     }
+    require(ra.list == nullptr, LO_LOGIC_ERROR, "tile-list fill needs the FP32 path");
 #define LO_RADIUS_CASE(S)                                                                        \
     case S:                                                                                      \
         radius_kernel<S, FILL><<<blocks, kRadiusThreads, 0, ctx->stream>>>(t->tn, c->x, c->y,    \
@@ -160,23 +167,47 @@ static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
     LO_CHECK_LAUNCH();
 }
 
+// Records per tile for the fused count -> replay fill (32 buffers x 256 B = 8 KB per tile).
+constexpr u32 kRecCap = 32;
+
 static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded* c, int shape,
                              double r, const Queries& q, bool fingerprint) {
     require(t != nullptr && c != nullptr, LO_INVALID_ARGUMENT, "null tree or cloud");
     require(r > 0.0 && std::isfinite(r), LO_INVALID_ARGUMENT,
             "kernel radius must be positive and finite");
+    require(shape >= LO_SPHERE && shape <= LO_SQUARE, LO_INVALID_ARGUMENT, "unknown kernel shape");
     auto* out = new lo_csr;
     out->ctx = ctx;
     out->rows = q.m;
     cudaEvent_t e0, e1;
     LO_CUDA(cudaEventCreate(&e0));
     LO_CUDA(cudaEventCreate(&e1));
+    RecArgs ra;
+    u32* ovf = nullptr;
+    u32* ovf_n = nullptr;
     try {
         LO_CUDA(cudaEventRecord(e0, ctx->stream));
         out->counts = dalloc_t<u32>(ctx, q.m);
         out->offsets = dalloc_t<u64>(ctx, q.m + 1);
+        const u64 tiles = (q.m + 31) / 32;
+        static const bool no_fuse = std::getenv("LO_RADIUS_NO_FUSE") != nullptr;
+        if (q.m && !no_fuse && float_path(t, c, q, r)) {
+            try {
+                // one persistent block: records | rec_n[tiles] | overflow list[tiles] | ovf_n
+                const size_t rec_words = tiles * kRecCap * 64;
+                u32* base = static_cast<u32*>(arena(ctx, 4 * (rec_words + 2 * tiles + 1)));
+                ra.rec = base;
+                ra.rec_n = base + rec_words;
+                ra.cap = kRecCap;
+                ovf = ra.rec_n + tiles;
+                ovf_n = ovf + tiles;
+            } catch (const Error&) {  // not enough memory for the records: two-walk path
+                ra = RecArgs{};
+                ovf = ovf_n = nullptr;
+            }
+        }
         stage_begin(ctx, "radius_count");
-        if (q.m) launch_radius<false>(ctx, shape, t, c, q, r, out->counts, nullptr, nullptr);
+        if (q.m) launch_radius<false>(ctx, shape, t, c, q, r, out->counts, nullptr, nullptr, ra);
         stage_end(ctx);
         stage_begin(ctx, "radius_scan");
         exclusive_scan_u32_to_u64(ctx, out->counts, out->offsets, q.m);
@@ -184,8 +215,29 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
         out->total = read_scalar(ctx, out->offsets + q.m);
         out->indices = dalloc_t<u32>(ctx, out->total);
         stage_begin(ctx, "radius_fill");
-        if (q.m) launch_radius<true>(ctx, shape, t, c, q, r, nullptr, out->offsets, out->indices);
+        if (q.m && ra.rec) {
+            LO_CUDA(cudaMemsetAsync(ovf_n, 0, 4, ctx->stream));
+            const int rb = static_cast<int>(std::max<u64>(1, std::min<u64>((tiles + 3) / 4, ctx->sm_count * 16ull)));
+            radius_replay_kernel<<<rb, 128, 0, ctx->stream>>>(ra.rec, ra.cap, ra.rec_n, q.m, out->offsets,
+                                                            out->indices, ovf, ovf_n);
+            LO_CHECK_LAUNCH();
+            const u32 n_ovf = read_scalar(ctx, ovf_n);
+            static const bool debug = std::getenv("LO_DEBUG") != nullptr;
+            if (debug)
+                std::fprintf(stderr, "[lo] radius r=%g: %u of %llu tiles overflowed the %u-buffer records\n",
+                             r, n_ovf, static_cast<unsigned long long>(tiles), kRecCap);
+            if (n_ovf) {
+                RecArgs fb;
+                fb.list = ovf;
+                fb.list_n = n_ovf;
+                launch_radius<true>(ctx, shape, t, c, q, r, nullptr, out->offsets, out->indices, fb);
+            }
+        } else if (q.m) {
+            launch_radius<true>(ctx, shape, t, c, q, r, nullptr, out->offsets, out->indices);
+        }
         stage_end(ctx);
+        ra = RecArgs{};
+        ovf = ovf_n = nullptr;
         if (fingerprint) {
             out->fps = dalloc_t<u64>(ctx, q.m);
             stage_begin(ctx, "radius_digest");

@@ -52,7 +52,8 @@ __device__ __forceinline__ void process_buffer(PtShared& S, u32 fill, u32 qmask,
                                                const double* __restrict__ px,
                                                const double* __restrict__ py,
                                                const double* __restrict__ pz, double r,
-                                               double r2, u32* __restrict__ out_tile, u32& mine) {
+                                               double r2, u32* __restrict__ out_tile, u32& mine,
+                                               u32& mymask) {
     constexpr bool kPacked = SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE;
     // slots >= fill hold +INF (staged that way), so they are never members; a query that is
     // disjoint from every leaf of the buffer has d2_f >= near2_f >= t_hi for all its points,
@@ -88,14 +89,58 @@ __device__ __forceinline__ void process_buffer(PtShared& S, u32 fill, u32 qmask,
             if (h0 ^ in0) in0 = band_fix<SHAPE>(in0, h0 ^ in0, S, b, lane, idx, px, py, pz, r, r2);
             if (h1 ^ in1) in1 = band_fix<SHAPE>(in1, h1 ^ in1, S, b + 1, lane, idx, px, py, pz, r, r2);
         }
-        const u32 n0 = __popc(in0), n1 = __popc(in1);
         if (FILL) {
             const u32 c0 = __shfl_sync(~0u, mine, b);
             const u32 c1 = __shfl_sync(~0u, mine, b + 1);
             if ((in0 >> lane) & 1u) out_tile[c0 + __popc(in0 & lt)] = idx;
             if ((in1 >> lane) & 1u) out_tile[c1 + __popc(in1 & lt)] = idx;
+            mine += lane == b ? __popc(in0) : (lane == b + 1 ? __popc(in1) : 0u);
+        } else {
+            // lane L keeps query L's membership mask of this buffer (count + record)
+            mymask = lane == b ? in0 : (lane == b + 1 ? in1 : mymask);
         }
-        mine += lane == b ? n0 : (lane == b + 1 ? n1 : 0u);
+    }
+}
+
+constexpr u32 kRecOverflow = 0xffffffffu;
+
+// Fill pass by replay of the count pass's records: record b of a tile holds the 32 slot indices
+// of one processed buffer and, per query lane, its membership mask.  Query L's members of the
+// buffer go to consecutive CSR slots with one coalesced store; no walk, no re-tested points.
+__global__ void __launch_bounds__(128) radius_replay_kernel(const u32* __restrict__ rec, u32 rec_cap,
+                                                            const u32* __restrict__ rec_n, u64 m,
+                                                            const u64* __restrict__ offsets,
+                                                            u32* __restrict__ out,
+                                                            u32* __restrict__ overflow_list,
+                                                            u32* __restrict__ overflow_n) {
+    const int lane = threadIdx.x & 31;
+    const u32 lt = (1u << lane) - 1u;
+    const u64 ntiles = (m + 31) / 32;
+    for (u64 tile = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; tile < ntiles;
+         tile += (static_cast<u64>(gridDim.x) * blockDim.x) >> 5) {
+        const u32 n = rec_n[tile];
+        if (n == kRecOverflow) {
+            if (lane == 0) overflow_list[atomicAdd(overflow_n, 1u)] = static_cast<u32>(tile);
+            continue;
+        }
+        const u64 qi = tile * 32 + lane;
+        const u64 tbase = offsets[tile * 32];
+        u32* out_tile = out + tbase;
+        u32 cursor = qi < m ? static_cast<u32>(offsets[qi] - tbase) : 0u;
+        const u32* R = rec + tile * rec_cap * 64;
+        for (u32 b = 0; b < n; ++b, R += 64) {
+            const u32 idx = R[lane];
+            const u32 mk = R[32 + lane];
+            unsigned nz = __ballot_sync(~0u, mk != 0);
+            while (nz) {
+                const int L = __ffs(nz) - 1;
+                nz &= nz - 1;
+                const u32 mL = __shfl_sync(~0u, mk, L);
+                const u32 cL = __shfl_sync(~0u, cursor, L);
+                if ((mL >> lane) & 1u) out_tile[cL + __popc(mL & lt)] = idx;
+            }
+            cursor += __popc(mk);
+        }
     }
 }
 
@@ -104,11 +149,12 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
     const TNodeF* __restrict__ tf, const float4* __restrict__ pf, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, Queries q, FloatTest ft,
     float compact, double r, double r2, u32* __restrict__ counts, const u64* __restrict__ offsets,
-    u32* __restrict__ out, u64* tile_counter) {
+    u32* __restrict__ out, u64* tile_counter, u32* __restrict__ rec, u32 rec_cap,
+    u32* __restrict__ rec_n, const u32* __restrict__ tile_list, u64 list_n) {
     __shared__ PtShared shared_s[kPtWarps];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     PtShared& S = shared_s[w];
-    const u64 ntiles = (q.m + 31) / 32;
+    const u64 ntiles = tile_list ? list_n : (q.m + 31) / 32;
     const int cl = lane & 7, grp = lane >> 3;
     constexpr bool kSq = SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE;
     const float lo_thr = kSq ? ft.t_lo : ft.r_lo;
@@ -118,6 +164,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
         if (lane == 0) tile = atomicAdd(reinterpret_cast<unsigned long long*>(tile_counter), 1ull);
         tile = __shfl_sync(~0u, tile, 0);
         if (tile >= ntiles) break;
+        if (tile_list) tile = tile_list[tile];  // fill fallback for tiles the records missed
         const u64 qi = tile * 32 + lane;
         const bool active = qi < q.m;
         double cx = 0.0, cy = 0.0, cz = 0.0;
@@ -153,6 +200,24 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
         }
         const bool gcompact = fmaxf(fmaxf(gh[0] - gl[0], gh[1] - gl[1]), gh[2] - gl[2]) <= compact;
         u32 fill = 0, qmask = 0;  // buffer occupancy and interested queries (warp-uniform)
+        u32 nrec = 0;             // count pass: buffers recorded for the replay
+        u32* rec_tile = rec ? rec + tile * rec_cap * 64 : nullptr;
+        auto flush = [&]() {
+            u32 mymask = 0;
+            process_buffer<SHAPE, FILL>(S, fill, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2,
+                                        out_tile, mine, mymask);
+            if (!FILL) {
+                mine += __popc(mymask);
+                if (rec_tile) {
+                    if (nrec < rec_cap) {
+                        u32* R = rec_tile + nrec * 64;
+                        R[lane] = __float_as_uint(S.buf[lane].w);
+                        R[32 + lane] = mymask;
+                    }
+                    ++nrec;
+                }
+            }
+        };
         int sp = 1;
         if (lane == 0) S.stack[0] = 0;
         __syncwarp();
@@ -196,8 +261,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
                 base += take;
                 if (fill == 32) {
                     __syncwarp();
-                    process_buffer<SHAPE, FILL>(S, fill, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2,
-                                                out_tile, mine);
+                    flush();
                     fill = 0;
                     qmask = 0;
                 }
@@ -207,10 +271,10 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             // partial last buffer: pad with never-member slots
             if (static_cast<u32>(lane) >= fill) S.buf[lane] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
             __syncwarp();
-            process_buffer<SHAPE, FILL>(S, fill, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2, out_tile,
-                                        mine);
+            flush();
         }
         if (!FILL && active) counts[qi] = mine;
+        if (!FILL && rec && lane == 0) rec_n[tile] = nrec <= rec_cap ? nrec : kRecOverflow;
         __syncwarp();
     }
 }
