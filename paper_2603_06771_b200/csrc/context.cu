@@ -56,6 +56,8 @@ void* arena(lo_context* ctx, size_t bytes) {
         ctx->arena_bytes = 0;
     }
     const size_t want = bytes + bytes / 4;  // headroom: a slightly larger batch reuses it
+    static const bool debug = std::getenv("LO_DEBUG") != nullptr;
+    if (debug) std::fprintf(stderr, "[lo] arena grows to %zu bytes\n", want);
     cudaError_t e = cudaMalloc(&ctx->arena, want);
     if (e != cudaSuccess) {
         cudaGetLastError();

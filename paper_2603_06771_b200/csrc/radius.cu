@@ -105,9 +105,7 @@ __global__ void counts_from_offsets(const u64* __restrict__ offsets, u64 m, u32*
 }
 
 struct RecArgs {  // count-pass records for the replay fill (radius_pt.cuh)
-    u32* rec = nullptr;
-    u32 cap = 0;
-    u32* rec_n = nullptr;
+    RecPool rp;
     const u32* list = nullptr;  // fill fallback: only these tiles
     u64 list_n = 0;
 };
@@ -135,7 +133,7 @@ static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
     case S:                                                                                     \
         radius_pt_kernel<S, FILL><<<pblocks, kPtThreads, 0, ctx->stream>>>(                    \
             t->tf, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, counts, offsets, out,        \
-            counter, ra.rec, ra.cap, ra.rec_n, ra.list, ra.list_n);                             \
+            counter, ra.rp, ra.list, ra.list_n);                                                \
         break;
         switch (shape) {
             LO_RADIUS_F(LO_SPHERE)
@@ -167,8 +165,8 @@ static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
     LO_CHECK_LAUNCH();
 }
 
-// Records per tile for the fused count -> replay fill (32 buffers x 256 B = 8 KB per tile).
-constexpr u32 kRecCap = 32;
+// Max records per tile for the fused count -> replay fill (64 buffers x 256 B = 16 KB).
+constexpr u32 kRecCap = 64;
 
 static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded* c, int shape,
                              double r, const Queries& q, bool fingerprint) {
@@ -193,14 +191,31 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
         static const bool no_fuse = std::getenv("LO_RADIUS_NO_FUSE") != nullptr;
         if (q.m && !no_fuse && float_path(t, c, q, r)) {
             try {
-                // one persistent block: records | rec_n[tiles] | overflow list[tiles] | ovf_n
-                const size_t rec_words = tiles * kRecCap * 64;
-                u32* base = static_cast<u32*>(arena(ctx, 4 * (rec_words + 2 * tiles + 1)));
-                ra.rec = base;
-                ra.rec_n = base + rec_words;
-                ra.cap = kRecCap;
-                ovf = ra.rec_n + tiles;
+                // one persistent block: rec_off[tiles] u64 | alloc u64 | rec_n[tiles] |
+                // overflow list[tiles] | ovf_n | pool (records of 256 B).  The pool is sized for
+                // the worst case (kRecCap per tile) within a quarter of the free memory; tiles that
+                // find it exhausted fall back to the fill walk.
+                const u64 head = 8 * (tiles + 1) + 4 * (2 * tiles + 1);
+                u64 recs = tiles * kRecCap;
+                if (head + 16 + recs * 256 > ctx->arena_bytes) {  // growing: respect free memory
+                    size_t free_b = 0, total_b = 0;
+                    LO_CUDA(cudaMemGetInfo(&free_b, &total_b));
+                    const u64 budget = (free_b + ctx->arena_bytes) / 4;
+                    recs = std::min<u64>(recs, budget > head ? (budget - head) / 256 : 0);
+                } else {  // reuse whatever the arena holds
+                    recs = (ctx->arena_bytes - head - 16) / 256;
+                }
+                recs = std::max<u64>(recs, kRecChunk * 2);
+                unsigned char* base = static_cast<unsigned char*>(arena(ctx, head + 16 + recs * 256));
+                ra.rp.rec_off = reinterpret_cast<u64*>(base);
+                ra.rp.alloc = ra.rp.rec_off + tiles;
+                ra.rp.rec_n = reinterpret_cast<u32*>(ra.rp.alloc + 1);
+                ovf = ra.rp.rec_n + tiles;
                 ovf_n = ovf + tiles;
+                ra.rp.pool = reinterpret_cast<u32*>(base + ((head + 15) / 16) * 16);
+                ra.rp.pool_recs = recs;
+                ra.rp.cap = kRecCap;
+                LO_CUDA(cudaMemsetAsync(ra.rp.alloc, 0, 8, ctx->stream));
             } catch (const Error&) {  // not enough memory for the records: two-walk path
                 ra = RecArgs{};
                 ovf = ovf_n = nullptr;
@@ -215,11 +230,18 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
         out->total = read_scalar(ctx, out->offsets + q.m);
         out->indices = dalloc_t<u32>(ctx, out->total);
         stage_begin(ctx, "radius_fill");
-        if (q.m && ra.rec) {
+        if (q.m && ra.rp.pool) {
             LO_CUDA(cudaMemsetAsync(ovf_n, 0, 4, ctx->stream));
-            const int rb = static_cast<int>(std::max<u64>(1, std::min<u64>((tiles + 3) / 4, ctx->sm_count * 16ull)));
-            radius_replay_kernel<<<rb, 128, 0, ctx->stream>>>(ra.rec, ra.cap, ra.rec_n, q.m, out->offsets,
-                                                            out->indices, ovf, ovf_n);
+            const int rb = static_cast<int>(std::max<u64>(
+                1, std::min<u64>((tiles + kReplayWarps - 1) / kReplayWarps, ctx->sm_count * 16ull)));
+            // short rows: buffer-major stores stay line-local; long rows: row-major so every
+            // output line completes while hot (measured crossover ~ 64 members per row)
+            if (out->total < 64ull * q.m)
+                radius_replay_bm_kernel<<<rb, 128, 0, ctx->stream>>>(ra.rp, q.m, out->offsets, out->indices,
+                                                                    ovf, ovf_n);
+            else
+                radius_replay_kernel<<<rb, 32 * kReplayWarps, 0, ctx->stream>>>(
+                    ra.rp, q.m, out->offsets, out->indices, ovf, ovf_n);
             LO_CHECK_LAUNCH();
             const u32 n_ovf = read_scalar(ctx, ovf_n);
             static const bool debug = std::getenv("LO_DEBUG") != nullptr;

@@ -103,22 +103,39 @@ __device__ __forceinline__ void process_buffer(PtShared& S, u32 fill, u32 qmask,
 }
 
 constexpr u32 kRecOverflow = 0xffffffffu;
+constexpr u32 kRecChunk = 512;  // records per warp chunk (128 KB)
+
+// Count-pass records, packed: each warp takes chunks of kRecChunk records from a bump
+// allocator and appends its tiles' records contiguously; tile t's records start at record
+// rec_off[t] and number rec_n[t] (kRecOverflow: not recorded -> fill-walk fallback).
+struct RecPool {
+    u32* pool = nullptr;    // 64 words per record: 32 slot indices, 32 query masks
+    u64 pool_recs = 0;
+    u64* alloc = nullptr;   // bump counter (records)
+    u32 cap = 0;            // max records per tile
+    u32* rec_n = nullptr;   // [tiles]
+    u64* rec_off = nullptr; // [tiles]
+};
 
 // Fill pass by replay of the count pass's records: record b of a tile holds the 32 slot indices
-// of one processed buffer and, per query lane, its membership mask.  Query L's members of the
-// buffer go to consecutive CSR slots with one coalesced store; no walk, no re-tested points.
-__global__ void __launch_bounds__(128) radius_replay_kernel(const u32* __restrict__ rec, u32 rec_cap,
-                                                            const u32* __restrict__ rec_n, u64 m,
-                                                            const u64* __restrict__ offsets,
-                                                            u32* __restrict__ out,
-                                                            u32* __restrict__ overflow_list,
-                                                            u32* __restrict__ overflow_n) {
+// of one processed buffer and, per query lane, its membership mask.  The tile's records are
+// staged in shared memory and the rows are written one after the other: row L takes its members
+// of buffer b with one coalesced store at consecutive CSR slots, so every output line is
+// completed while it is hot in L2 (writing buffer-major across all 32 rows left ~10^4 tiles'
+// lines half-written and cost read-modify-write traffic).  No walk, no re-tested points.
+constexpr int kReplayWarps = 4;
+
+// Buffer-major replay for short rows (small radii): per record, one coalesced store per query
+// with members; the few, short rows of a tile stay within a handful of lines.
+__global__ void __launch_bounds__(128) radius_replay_bm_kernel(
+    RecPool rp, u64 m, const u64* __restrict__ offsets, u32* __restrict__ out,
+    u32* __restrict__ overflow_list, u32* __restrict__ overflow_n) {
     const int lane = threadIdx.x & 31;
     const u32 lt = (1u << lane) - 1u;
     const u64 ntiles = (m + 31) / 32;
     for (u64 tile = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; tile < ntiles;
          tile += (static_cast<u64>(gridDim.x) * blockDim.x) >> 5) {
-        const u32 n = rec_n[tile];
+        const u32 n = rp.rec_n[tile];
         if (n == kRecOverflow) {
             if (lane == 0) overflow_list[atomicAdd(overflow_n, 1u)] = static_cast<u32>(tile);
             continue;
@@ -127,10 +144,10 @@ __global__ void __launch_bounds__(128) radius_replay_kernel(const u32* __restric
         const u64 tbase = offsets[tile * 32];
         u32* out_tile = out + tbase;
         u32 cursor = qi < m ? static_cast<u32>(offsets[qi] - tbase) : 0u;
-        const u32* R = rec + tile * rec_cap * 64;
+        const u32* R = rp.pool + rp.rec_off[tile] * 64;
         for (u32 b = 0; b < n; ++b, R += 64) {
-            const u32 idx = R[lane];
-            const u32 mk = R[32 + lane];
+            const u32 idx = __ldg(R + lane);
+            const u32 mk = __ldg(R + 32 + lane);
             unsigned nz = __ballot_sync(~0u, mk != 0);
             while (nz) {
                 const int L = __ffs(nz) - 1;
@@ -144,13 +161,70 @@ __global__ void __launch_bounds__(128) radius_replay_kernel(const u32* __restric
     }
 }
 
+__global__ void __launch_bounds__(32 * kReplayWarps) radius_replay_kernel(
+    RecPool rp, u64 m, const u64* __restrict__ offsets, u32* __restrict__ out,
+    u32* __restrict__ overflow_list, u32* __restrict__ overflow_n) {
+    const u32* __restrict__ rec_n = rp.rec_n;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const u32 lt = (1u << lane) - 1u;
+    const u64 ntiles = (m + 31) / 32;
+    for (u64 tile = static_cast<u64>(blockIdx.x) * kReplayWarps + w; tile < ntiles;
+         tile += static_cast<u64>(gridDim.x) * kReplayWarps) {
+        const u32 n = rec_n[tile];
+        if (n == kRecOverflow) {
+            if (lane == 0) overflow_list[atomicAdd(overflow_n, 1u)] = static_cast<u32>(tile);
+            continue;
+        }
+        const u64 qi = tile * 32 + lane;
+        const u64 tbase = offsets[tile * 32];
+        u32* out_tile = out + tbase;
+        const u32 start = qi < m ? static_cast<u32>(offsets[qi] - tbase) : 0u;
+        const u32* R = rp.pool + rp.rec_off[tile] * 64;
+        // row by row; lane b holds row L's masks of buffers b and b + 32 (n <= 64), a warp scan
+        // of their popcounts gives each buffer's CSR start, so the write loop below only needs
+        // shuffles and independent index loads
+        const u32 total = qi < m ? static_cast<u32>(offsets[qi + 1] - offsets[qi]) : 0u;
+        unsigned rows = __ballot_sync(~0u, total != 0);
+        while (rows) {
+            const int L = __ffs(rows) - 1;
+            rows &= rows - 1;
+            const u32 c0 = __shfl_sync(~0u, start, L);
+            const u32 ma = static_cast<u32>(lane) < n ? __ldg(R + lane * 64 + 32 + L) : 0u;
+            const u32 mb = static_cast<u32>(lane) + 32 < n ? __ldg(R + (lane + 32) * 64 + 32 + L) : 0u;
+            const u32 ca = __popc(ma), cb = __popc(mb);
+            u32 sa = ca, sb = cb;  // inclusive scans
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 ta = __shfl_up_sync(~0u, sa, o), tb = __shfl_up_sync(~0u, sb, o);
+                if (lane >= o) sa += ta, sb += tb;
+            }
+            const u32 tot_a = __shfl_sync(~0u, sa, 31);
+            const u32 pa = c0 + sa - ca, pb = c0 + tot_a + sb - cb;  // exclusive starts
+            for (int half = 0; half < 2; ++half) {
+                const u32 mine_m = half ? mb : ma;
+                const u32 mine_p = half ? pb : pa;
+                unsigned nz = __ballot_sync(~0u, mine_m != 0);
+                const u32* Rh = R + half * 32 * 64;
+                while (nz) {
+                    const int b = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    const u32 mL = __shfl_sync(~0u, mine_m, b);
+                    const u32 pL = __shfl_sync(~0u, mine_p, b);
+                    const u32 idx = __ldg(Rh + b * 64 + lane);
+                    if ((mL >> lane) & 1u) out_tile[pL + __popc(mL & lt)] = idx;
+                }
+            }
+        }
+    }
+}
+
 template <int SHAPE, bool FILL>
 __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
     const TNodeF* __restrict__ tf, const float4* __restrict__ pf, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, Queries q, FloatTest ft,
     float compact, double r, double r2, u32* __restrict__ counts, const u64* __restrict__ offsets,
-    u32* __restrict__ out, u64* tile_counter, u32* __restrict__ rec, u32 rec_cap,
-    u32* __restrict__ rec_n, const u32* __restrict__ tile_list, u64 list_n) {
+    u32* __restrict__ out, u64* tile_counter, RecPool rp, const u32* __restrict__ tile_list,
+    u64 list_n) {
     __shared__ PtShared shared_s[kPtWarps];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     PtShared& S = shared_s[w];
@@ -159,12 +233,23 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
     constexpr bool kSq = SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE;
     const float lo_thr = kSq ? ft.t_lo : ft.r_lo;
     const float hi_thr = kSq ? ft.t_hi : ft.r_hi;
+    u64 chunk_base = 0;  // count pass: this warp's current record chunk (in records)
+    u32 chunk_left = 0;
     for (;;) {
         u64 tile = 0;
         if (lane == 0) tile = atomicAdd(reinterpret_cast<unsigned long long*>(tile_counter), 1ull);
         tile = __shfl_sync(~0u, tile, 0);
         if (tile >= ntiles) break;
         if (tile_list) tile = tile_list[tile];  // fill fallback for tiles the records missed
+        if (!FILL && rp.pool && chunk_left < rp.cap) {
+            // a fresh chunk so this tile's records stay contiguous
+            u64 base = 0;
+            if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long*>(rp.alloc),
+                                            static_cast<unsigned long long>(kRecChunk));
+            base = __shfl_sync(~0u, base, 0);
+            chunk_base = base;
+            chunk_left = base + kRecChunk <= rp.pool_recs ? kRecChunk : 0u;
+        }
         const u64 qi = tile * 32 + lane;
         const bool active = qi < q.m;
         double cx = 0.0, cy = 0.0, cz = 0.0;
@@ -201,7 +286,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
         const bool gcompact = fmaxf(fmaxf(gh[0] - gl[0], gh[1] - gl[1]), gh[2] - gl[2]) <= compact;
         u32 fill = 0, qmask = 0;  // buffer occupancy and interested queries (warp-uniform)
         u32 nrec = 0;             // count pass: buffers recorded for the replay
-        u32* rec_tile = rec ? rec + tile * rec_cap * 64 : nullptr;
+        u32* rec_tile = (!FILL && rp.pool && chunk_left >= rp.cap) ? rp.pool + chunk_base * 64 : nullptr;
         auto flush = [&]() {
             u32 mymask = 0;
             process_buffer<SHAPE, FILL>(S, fill, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2,
@@ -209,7 +294,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             if (!FILL) {
                 mine += __popc(mymask);
                 if (rec_tile) {
-                    if (nrec < rec_cap) {
+                    if (nrec < rp.cap) {
                         u32* R = rec_tile + nrec * 64;
                         R[lane] = __float_as_uint(S.buf[lane].w);
                         R[32 + lane] = mymask;
@@ -274,7 +359,17 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             flush();
         }
         if (!FILL && active) counts[qi] = mine;
-        if (!FILL && rec && lane == 0) rec_n[tile] = nrec <= rec_cap ? nrec : kRecOverflow;
+        if (!FILL && rp.pool) {
+            const bool ok = rec_tile && nrec <= rp.cap;
+            if (lane == 0) {
+                rp.rec_n[tile] = ok ? nrec : kRecOverflow;
+                rp.rec_off[tile] = chunk_base;
+            }
+            if (ok) {
+                chunk_base += nrec;
+                chunk_left -= nrec;
+            }
+        }
         __syncwarp();
     }
 }
