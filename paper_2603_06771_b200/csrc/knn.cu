@@ -267,8 +267,7 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
         const bool use_float = q.f && t->tf && c->pf;
         const size_t per_warp_heap = static_cast<size_t>(kh) * 32 * 12;
         const size_t per_warp_fixed =
-            use_float ? sizeof(u32) * kStackCap + 4 * 32 + 16 * 32 + 16 * 16 + 8 * 16 + 4 * 32
-                      : sizeof(u32) * kStackCap + 96 * sizeof(double);
+            use_float ? kKnnFixed : sizeof(u32) * kStackCap + 96 * sizeof(double);
         const bool global_heap = per_warp_heap + per_warp_fixed > static_cast<size_t>(kKnnSmemBudget);
         int warps = 4;
         if (!global_heap)
@@ -282,7 +281,8 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
             1, std::min<u64>((tiles + warps - 1) / warps, static_cast<u64>(ctx->sm_count) * per_sm)));
         stage_begin(ctx, "knn");
         if (q.m && use_float) {
-            const double E = std::ldexp(std::max(c->bmax, q.bmax), -23);
+            float E = static_cast<float>(std::ldexp(std::max(c->bmax, q.bmax), -23));
+            E = std::nextafter(E, INFINITY);  // round up
             const u32 seed_half = std::max<u32>(16, kh);
             u64* counter = dalloc_t<u64>(ctx, 1);
             LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));

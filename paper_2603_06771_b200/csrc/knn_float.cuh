@@ -25,25 +25,40 @@ struct KnnSmem {
     float4* pa;     // staged candidate pairs (x0, x1, y0, y1)
     float2* pb;     // (z0, z1)
     u32* pidx;      // staged candidate indices
+    double* pd;     // staged candidate FP64 coordinates (x, y, z per slot)
 };
 
-__device__ __forceinline__ float knn_threshold(double w, double E) {
-    const double u = 1.1920928955078125e-07;  // 2^-23
-    const double sw = sqrt(w);
-    const double dd = 2.0 * E + u * 2.0 * sw;
-    const double M = 1.5 * (12.0 * u * w + 4.0 * 1.7320508075688772 * sw * dd + 3.0 * dd * dd +
-                            4.0e-15 * w);
-    return __double2float_ru(w + M);
+// Per-warp shared layout of knn_float_kernel (bytes): pd | stack | tq | qf | pa | pb | pidx
+constexpr size_t kKnnOffPd = 0;
+constexpr size_t kKnnOffStack = kKnnOffPd + 32 * 3 * 8;
+constexpr size_t kKnnOffTq = kKnnOffStack + 4 * kStackCap;
+constexpr size_t kKnnOffQf = kKnnOffTq + 4 * 32;
+constexpr size_t kKnnOffPa = kKnnOffQf + 16 * 32;
+constexpr size_t kKnnOffPb = kKnnOffPa + 16 * 16;
+constexpr size_t kKnnOffPidx = kKnnOffPb + 8 * 16;
+constexpr size_t kKnnFixed = kKnnOffPidx + 4 * 32;
+
+// T(w) = w + M(w) as an FP32 upper bound.  Evaluated in FP32 with every rounding directed up
+// and a factor-3 slack on M (a larger T only admits more candidates to the exact FP64 test, so
+// any overestimate is safe).
+__device__ __forceinline__ float knn_threshold(double w, float E) {
+    const float u = 1.1920928955078125e-07f;  // 2^-23
+    const float wf = __double2float_ru(w);
+    const float sw = __fsqrt_ru(wf);
+    const float dd = __fmaf_ru(2.0f * u, sw, 2.0f * E);
+    float M = __fmul_ru(12.0f * u, wf);
+    M = __fmaf_ru(4.0f * 1.7320509f * sw, dd, M);
+    M = __fmaf_ru(3.0f * dd, dd, M);
+    M = __fmaf_ru(4.0e-15f, wf, M);
+    return __fmaf_ru(3.0f, M, wf);
 }
 
 // One candidate j (global index g, FP32 squared distance v) for this lane.
 __device__ __forceinline__ void knn_offer(LaneHeap& heap, u32 k, double& worst_d, u32& worst_i,
-                                          float& T, double E, float v, u32 g, double cx, double cy,
-                                          double cz, const double* __restrict__ px,
-                                          const double* __restrict__ py,
-                                          const double* __restrict__ pz) {
+                                          float& T, float E, float v, u32 g, double cx, double cy,
+                                          double cz, const double* pxyz) {
     if (v > T) return;
-    const double d = point_dist_sq(px[g], py[g], pz[g], cx, cy, cz);
+    const double d = point_dist_sq(pxyz[0], pxyz[1], pxyz[2], cx, cy, cz);
     if (heap.size < k) {
         heap.push(d, g);
         if (heap.size == k) {
@@ -62,10 +77,8 @@ __device__ __forceinline__ void knn_offer(LaneHeap& heap, u32 k, double& worst_d
 // Tests the `cnt` staged candidates against this lane's query (pairs, packed FP32).
 __device__ __forceinline__ void knn_chunk(const KnnSmem& S, u32 cnt, bool active, u64 QX, u64 QY,
                                           u64 QZ, LaneHeap& heap, u32 k, double& worst_d,
-                                          u32& worst_i, float& T, double E, double cx, double cy,
-                                          double cz, const double* __restrict__ px,
-                                          const double* __restrict__ py,
-                                          const double* __restrict__ pz, u32 skip_lo, u32 skip_hi) {
+                                          u32& worst_i, float& T, float E, double cx, double cy,
+                                          double cz, u32 skip_lo, u32 skip_hi) {
     if (!active) return;
     const u32 npairs = (cnt + 1) >> 1;
     for (u32 pp = 0; pp < npairs; ++pp) {
@@ -82,29 +95,35 @@ __device__ __forceinline__ void knn_chunk(const KnnSmem& S, u32 cnt, bool active
         if (v0 <= T) {
             const u32 g = S.pidx[2 * pp];
             if (g < skip_lo || g >= skip_hi)
-                knn_offer(heap, k, worst_d, worst_i, T, E, v0, g, cx, cy, cz, px, py, pz);
+                knn_offer(heap, k, worst_d, worst_i, T, E, v0, g, cx, cy, cz, S.pd + 6 * pp);
         }
         if (2 * pp + 1 < cnt && v1 <= T) {
             const u32 g = S.pidx[2 * pp + 1];
             if (g < skip_lo || g >= skip_hi)
-                knn_offer(heap, k, worst_d, worst_i, T, E, v1, g, cx, cy, cz, px, py, pz);
+                knn_offer(heap, k, worst_d, worst_i, T, E, v1, g, cx, cy, cz, S.pd + 6 * pp + 3);
         }
     }
 }
 
-// Stage points [base, base + cnt) (cnt <= 32) of the sorted cloud as FP32 pairs.
-__device__ __forceinline__ void knn_stage(const KnnSmem& S, const float4* __restrict__ pf, u32 base,
-                                          u32 cnt, int lane) {
+// Stage points [base, base + cnt) (cnt <= 32) of the sorted cloud: FP32 pairs for the filter,
+// FP64 coordinates for the exact test of the candidates that pass it.
+__device__ __forceinline__ void knn_stage(const KnnSmem& S, const float4* __restrict__ pf,
+                                          const double* __restrict__ px, const double* __restrict__ py,
+                                          const double* __restrict__ pz, u32 base, u32 cnt, int lane) {
     __syncwarp();
     if (static_cast<u32>(lane) < cnt) {
-        const float4 p = __ldg(pf + base + lane);
+        const u32 g = base + lane;
+        const float4 p = __ldg(pf + g);
         float* a = reinterpret_cast<float*>(S.pa);
         float* b = reinterpret_cast<float*>(S.pb);
         const int pp = lane >> 1, h = lane & 1;
         a[4 * pp + h] = p.x;
         a[4 * pp + 2 + h] = p.y;
         b[2 * pp + h] = p.z;
-        S.pidx[lane] = base + lane;
+        S.pidx[lane] = g;
+        S.pd[3 * lane] = __ldg(px + g);
+        S.pd[3 * lane + 1] = __ldg(py + g);
+        S.pd[3 * lane + 2] = __ldg(pz + g);
     }
     __syncwarp();
 }
@@ -115,22 +134,21 @@ template <bool GLOBAL_HEAP>
 __global__ void __launch_bounds__(128) knn_float_kernel(
     const TNodeF* __restrict__ tf, const float4* __restrict__ pf, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, u64 npoints, Queries q,
-    i64 seed_base, u32 seed_half, double E, u32 k, u32* __restrict__ out_idx,
+    i64 seed_base, u32 seed_half, float E, u32 k, u32* __restrict__ out_idx,
     double* __restrict__ out_dist, double* __restrict__ gheap_d, u32* __restrict__ gheap_i,
     u64* tile_counter) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warps = blockDim.x >> 5;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // per-warp shared layout (fixed part): stack, tq[32], qf[32], pa[16], pb[16], pidx[32]
-    constexpr size_t kFixed = sizeof(u32) * kKnnFloatStack + 4 * 32 + 16 * 32 + 16 * 16 + 8 * 16 + 4 * 32;
-    unsigned char* mine = smem + w * kFixed;
+    unsigned char* mine = smem + w * kKnnFixed;
     KnnSmem S;
-    S.stack = reinterpret_cast<u32*>(mine);
-    S.tq = reinterpret_cast<float*>(mine + sizeof(u32) * kKnnFloatStack);
-    S.qf = reinterpret_cast<float4*>(mine + sizeof(u32) * kKnnFloatStack + 4 * 32);
-    S.pa = reinterpret_cast<float4*>(mine + sizeof(u32) * kKnnFloatStack + 4 * 32 + 16 * 32);
-    S.pb = reinterpret_cast<float2*>(mine + sizeof(u32) * kKnnFloatStack + 4 * 32 + 16 * 32 + 16 * 16);
-    S.pidx = reinterpret_cast<u32*>(mine + sizeof(u32) * kKnnFloatStack + 4 * 32 + 16 * 32 + 16 * 16 + 8 * 16);
+    S.pd = reinterpret_cast<double*>(mine + kKnnOffPd);
+    S.stack = reinterpret_cast<u32*>(mine + kKnnOffStack);
+    S.tq = reinterpret_cast<float*>(mine + kKnnOffTq);
+    S.qf = reinterpret_cast<float4*>(mine + kKnnOffQf);
+    S.pa = reinterpret_cast<float4*>(mine + kKnnOffPa);
+    S.pb = reinterpret_cast<float2*>(mine + kKnnOffPb);
+    S.pidx = reinterpret_cast<u32*>(mine + kKnnOffPidx);
     double* hd;
     u32* hi;
     if (GLOBAL_HEAP) {
@@ -138,7 +156,7 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
         hd = gheap_d + slot * k * 32 + lane;
         hi = gheap_i + slot * k * 32 + lane;
     } else {
-        double* heaps_d = reinterpret_cast<double*>(smem + warps * kFixed);
+        double* heaps_d = reinterpret_cast<double*>(smem + warps * kKnnFixed);
         u32* heaps_i = reinterpret_cast<u32*>(heaps_d + static_cast<u64>(warps) * k * 32);
         hd = heaps_d + static_cast<u64>(w) * k * 32 + lane;
         hi = heaps_i + static_cast<u64>(w) * k * 32 + lane;
@@ -179,9 +197,9 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
             skip_hi = static_cast<u32>(hi_);
             for (u32 b = skip_lo; b < skip_hi; b += 32) {
                 const u32 cnt = min(32u, skip_hi - b);
-                knn_stage(S, pf, b, cnt, lane);
+                knn_stage(S, pf, px, py, pz, b, cnt, lane);
                 knn_chunk(S, cnt, active, QX, QY, QZ, heap, k, worst_d, worst_i, T, E, cx, cy, cz,
-                          px, py, pz, 0u, 0u);
+                          0u, 0u);
             }
         }
 
@@ -229,9 +247,9 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
             if (!__any_sync(~0u, want)) continue;
             for (u32 b = nd.begin; b < nd.end; b += 32) {
                 const u32 cnt = min(32u, nd.end - b);
-                knn_stage(S, pf, b, cnt, lane);
-                knn_chunk(S, cnt, want, QX, QY, QZ, heap, k, worst_d, worst_i, T, E, cx, cy, cz, px,
-                          py, pz, skip_lo, skip_hi);
+                knn_stage(S, pf, px, py, pz, b, cnt, lane);
+                knn_chunk(S, cnt, want, QX, QY, QZ, heap, k, worst_d, worst_i, T, E, cx, cy, cz,
+                          skip_lo, skip_hi);
             }
         }
 
