@@ -239,9 +239,19 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
             if (out->total < 64ull * q.m)
                 radius_replay_bm_kernel<<<rb, 128, 0, ctx->stream>>>(ra.rp, q.m, out->offsets, out->indices,
                                                                     ovf, ovf_n);
-            else
-                radius_replay_kernel<<<rb, 32 * kReplayWarps, 0, ctx->stream>>>(
+            else {
+                static const bool attr = [] {
+                    LO_CUDA(cudaFuncSetAttribute(radius_replay_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(kReplaySmem)));
+                    return true;
+                }();
+                (void)attr;
+                const int rr = static_cast<int>(std::max<u64>(
+                    1, std::min<u64>((tiles + kReplayWarps - 1) / kReplayWarps, ctx->sm_count * 6ull)));
+                radius_replay_kernel<<<rr, 32 * kReplayWarps, kReplaySmem, ctx->stream>>>(
                     ra.rp, q.m, out->offsets, out->indices, ovf, ovf_n);
+            }
             LO_CHECK_LAUNCH();
             const u32 n_ovf = read_scalar(ctx, ovf_n);
             static const bool debug = std::getenv("LO_DEBUG") != nullptr;

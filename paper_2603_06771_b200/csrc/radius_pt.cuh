@@ -161,12 +161,25 @@ __global__ void __launch_bounds__(128) radius_replay_bm_kernel(
     }
 }
 
-__global__ void __launch_bounds__(32 * kReplayWarps) radius_replay_kernel(
+// Row-major replay for long rows.  The tile's records (read exactly once, streamed) are staged in
+// this warp's shared memory 32 at a time: slot indices as [b][32], masks as [b][33] so that lane b
+// reading row L's mask of buffer b is bank-conflict free.  Per row, lane b holds the row's mask of
+// buffer b; a warp scan of the popcounts gives every buffer's CSR start, and the write loop is two
+// shuffles, one shared load and one coalesced store per (row, buffer with members).
+constexpr u32 kReplayMaskStride = 33;
+constexpr size_t kReplayWarpWords = 32 * 32 + 32 * kReplayMaskStride;
+constexpr size_t kReplaySmem = kReplayWarps * kReplayWarpWords * 4;
+
+__global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_kernel(
     RecPool rp, u64 m, const u64* __restrict__ offsets, u32* __restrict__ out,
     u32* __restrict__ overflow_list, u32* __restrict__ overflow_n) {
+    extern __shared__ __align__(16) u32 replay_smem[];
     const u32* __restrict__ rec_n = rp.rec_n;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const u32 lt = (1u << lane) - 1u;
+    u32* I = replay_smem + w * kReplayWarpWords;  // [32][32] slot indices
+    u32* M = I + 32 * 32;                         // [32][33] per-row masks
+    const u32 ih = static_cast<u32>(__cvta_generic_to_shared(I + lane));
     const u64 ntiles = (m + 31) / 32;
     for (u64 tile = static_cast<u64>(blockIdx.x) * kReplayWarps + w; tile < ntiles;
          tile += static_cast<u64>(gridDim.x) * kReplayWarps) {
@@ -177,43 +190,68 @@ __global__ void __launch_bounds__(32 * kReplayWarps) radius_replay_kernel(
         }
         const u64 qi = tile * 32 + lane;
         const u64 tbase = offsets[tile * 32];
-        u32* out_tile = out + tbase;
-        const u32 start = qi < m ? static_cast<u32>(offsets[qi] - tbase) : 0u;
-        const u32* R = rp.pool + rp.rec_off[tile] * 64;
-        // row by row; lane b holds row L's masks of buffers b and b + 32 (n <= 64), a warp scan
-        // of their popcounts gives each buffer's CSR start, so the write loop below only needs
-        // shuffles and independent index loads
+        u32 cursor = qi < m ? static_cast<u32>(offsets[qi] - tbase) : 0u;  // lane L: row L
         const u32 total = qi < m ? static_cast<u32>(offsets[qi + 1] - offsets[qi]) : 0u;
-        unsigned rows = __ballot_sync(~0u, total != 0);
-        while (rows) {
-            const int L = __ffs(rows) - 1;
-            rows &= rows - 1;
-            const u32 c0 = __shfl_sync(~0u, start, L);
-            const u32 ma = static_cast<u32>(lane) < n ? __ldg(R + lane * 64 + 32 + L) : 0u;
-            const u32 mb = static_cast<u32>(lane) + 32 < n ? __ldg(R + (lane + 32) * 64 + 32 + L) : 0u;
-            const u32 ca = __popc(ma), cb = __popc(mb);
-            u32 sa = ca, sb = cb;  // inclusive scans
+        const unsigned rows_all = __ballot_sync(~0u, total != 0);
+        u32* out_tile = out + tbase;
+        asm("" : "+l"(out_tile));  // keep the row stores as 32-bit offsets from one base
+        const uint4* R4 = reinterpret_cast<const uint4*>(rp.pool + rp.rec_off[tile] * 64);
+        for (u32 h0 = 0; h0 < n; h0 += 32) {
+            const u32 nh = min(32u, n - h0);
+            const u32 nv = nh * 16;
+            const uint4* Rh = R4 + h0 * 16;
+            __syncwarp();
+            for (u32 i0 = 0; i0 < nv; i0 += 128) {
+                uint4 v[4];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const u32 ta = __shfl_up_sync(~0u, sa, o), tb = __shfl_up_sync(~0u, sb, o);
-                if (lane >= o) sa += ta, sb += tb;
+                for (int u = 0; u < 4; ++u) {
+                    const u32 i = i0 + u * 32 + lane;
+                    if (i < nv) v[u] = __ldcs(Rh + i);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const u32 i = i0 + u * 32 + lane;
+                    if (i < nv) {
+                        const u32 b = i >> 4, part = i & 15;
+                        if (part < 8) {
+                            *reinterpret_cast<uint4*>(I + b * 32 + part * 4) = v[u];
+                        } else {
+                            u32* d = M + b * kReplayMaskStride + (part - 8) * 4;
+                            d[0] = v[u].x, d[1] = v[u].y, d[2] = v[u].z, d[3] = v[u].w;
+                        }
+                    }
+                }
             }
-            const u32 tot_a = __shfl_sync(~0u, sa, 31);
-            const u32 pa = c0 + sa - ca, pb = c0 + tot_a + sb - cb;  // exclusive starts
-            for (int half = 0; half < 2; ++half) {
-                const u32 mine_m = half ? mb : ma;
-                const u32 mine_p = half ? pb : pa;
-                unsigned nz = __ballot_sync(~0u, mine_m != 0);
-                const u32* Rh = R + half * 32 * 64;
+            __syncwarp();
+            unsigned rows = rows_all;
+            u32 adv = 0;  // lane L: row L's members in this half
+            while (rows) {
+                const int L = __ffs(rows) - 1;
+                rows &= rows - 1;
+                const u32 c0 = __shfl_sync(~0u, cursor, L);
+                const u32 ma = static_cast<u32>(lane) < nh ? M[lane * kReplayMaskStride + L] : 0u;
+                const u32 ca = __popc(ma);
+                u32 sa = ca;  // inclusive scan
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const u32 ta = __shfl_up_sync(~0u, sa, o);
+                    if (lane >= o) sa += ta;
+                }
+                const u32 pa = c0 + sa - ca;  // exclusive start
+                const u32 tot = __shfl_sync(~0u, sa, 31);
+                if (lane == L) adv = tot;
+                unsigned nz = __ballot_sync(~0u, ma != 0);
                 while (nz) {
                     const int b = __ffs(nz) - 1;
                     nz &= nz - 1;
-                    const u32 mL = __shfl_sync(~0u, mine_m, b);
-                    const u32 pL = __shfl_sync(~0u, mine_p, b);
-                    const u32 idx = __ldg(Rh + b * 64 + lane);
-                    if ((mL >> lane) & 1u) out_tile[pL + __popc(mL & lt)] = idx;
+                    const u32 mL = __shfl_sync(~0u, ma, b);
+                    const u32 pL = __shfl_sync(~0u, pa, b);
+                    u32 idx;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(idx) : "r"(ih + b * 128) : "memory");
+                    if ((mL >> lane) & 1u) __stcg(out_tile + (pL + __popc(mL & lt)), idx);
                 }
             }
+            cursor += adv;
         }
     }
 }
