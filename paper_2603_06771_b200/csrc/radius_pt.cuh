@@ -223,33 +223,46 @@ __global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_kernel(
                 }
             }
             __syncwarp();
+            // rows two at a time: the two rows' scans and write loops are independent chains
             unsigned rows = rows_all;
             u32 adv = 0;  // lane L: row L's members in this half
             while (rows) {
-                const int L = __ffs(rows) - 1;
+                const int L1 = __ffs(rows) - 1;
                 rows &= rows - 1;
-                const u32 c0 = __shfl_sync(~0u, cursor, L);
-                const u32 ma = static_cast<u32>(lane) < nh ? M[lane * kReplayMaskStride + L] : 0u;
-                const u32 ca = __popc(ma);
-                u32 sa = ca;  // inclusive scan
+                const int L2 = rows ? __ffs(rows) - 1 : L1;
+                const bool two = rows != 0;
+                rows &= rows - 1;
+                const bool in = static_cast<u32>(lane) < nh;
+                const u32 m1 = in ? M[lane * kReplayMaskStride + L1] : 0u;
+                const u32 m2 = in && two ? M[lane * kReplayMaskStride + L2] : 0u;
+                const u32 a1 = __popc(m1), a2 = __popc(m2);
+                u32 s1 = a1, s2 = a2;  // inclusive scans
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
-                    const u32 ta = __shfl_up_sync(~0u, sa, o);
-                    if (lane >= o) sa += ta;
+                    const u32 t1 = __shfl_up_sync(~0u, s1, o), t2 = __shfl_up_sync(~0u, s2, o);
+                    if (lane >= o) s1 += t1, s2 += t2;
                 }
-                const u32 pa = c0 + sa - ca;  // exclusive start
-                const u32 tot = __shfl_sync(~0u, sa, 31);
-                if (lane == L) adv = tot;
-                unsigned nz = __ballot_sync(~0u, ma != 0);
-                while (nz) {
+                const u32 p1 = __shfl_sync(~0u, cursor, L1) + s1 - a1;  // exclusive starts
+                const u32 p2 = __shfl_sync(~0u, cursor, L2) + s2 - a2;
+                const u32 tot1 = __shfl_sync(~0u, s1, 31), tot2 = __shfl_sync(~0u, s2, 31);
+                if (lane == L1) adv = tot1;
+                if (two && lane == L2) adv = tot2;
+                unsigned nz1 = __ballot_sync(~0u, m1 != 0), nz2 = __ballot_sync(~0u, m2 != 0);
+                auto step = [&](unsigned& nz, u32 mk, u32 pk) {
                     const int b = __ffs(nz) - 1;
                     nz &= nz - 1;
-                    const u32 mL = __shfl_sync(~0u, ma, b);
-                    const u32 pL = __shfl_sync(~0u, pa, b);
+                    const u32 mL = __shfl_sync(~0u, mk, b);
+                    const u32 pL = __shfl_sync(~0u, pk, b);
                     u32 idx;
                     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(idx) : "r"(ih + b * 128) : "memory");
                     if ((mL >> lane) & 1u) __stcg(out_tile + (pL + __popc(mL & lt)), idx);
+                };
+                while (nz1 && nz2) {
+                    step(nz1, m1, p1);
+                    step(nz2, m2, p2);
                 }
+                while (nz1) step(nz1, m1, p1);
+                while (nz2) step(nz2, m2, p2);
             }
             cursor += adv;
         }
