@@ -28,6 +28,7 @@ struct PtShared {
     __align__(8) float qy[32];
     __align__(8) float qz[32];
     double qd[32][3];    // queries, FP64 (band decisions)
+    __align__(8) u32 msk[32];  // count pass: membership ballot of query L for the current buffer
 };
 
 // Decide band lanes exactly; returns the corrected membership ballot for query L.
@@ -62,7 +63,13 @@ __device__ __forceinline__ void process_buffer(PtShared& S, u32 fill, u32 qmask,
     const u32 idx = __float_as_uint(P.w);
     const u64 PX = pack2(P.x, P.x), PY = pack2(P.y, P.y), PZ = pack2(P.z, P.z);
     const u32 lt = (1u << lane) - 1u;
+    const u32 lo_bits = __float_as_uint(lo_thr);
+    const u32 band_bits = __float_as_uint(hi_thr) - lo_bits;
     u32 pm = (qmask | (qmask >> 1)) & 0x55555555u;  // bit 2p: pair p has an interested query
+    if (!FILL) {
+        S.msk[lane] = 0u;
+        __syncwarp();
+    }
     while (pm) {
         const int b = __ffs(pm) - 1;  // = 2p
         pm &= pm - 1;
@@ -83,9 +90,12 @@ __device__ __forceinline__ void process_buffer(PtShared& S, u32 fill, u32 qmask,
         }
         u32 in0 = __ballot_sync(~0u, v0 < lo_thr);
         u32 in1 = __ballot_sync(~0u, v1 < lo_thr);
-        const u32 h0 = __ballot_sync(~0u, v0 < hi_thr);
-        const u32 h1 = __ballot_sync(~0u, v1 < hi_thr);
-        if ((h0 ^ in0) | (h1 ^ in1)) {  // rare: band points, exact FP64 decides
+        // band lo <= v < hi as one unsigned range test on the bits (v >= 0 or NaN, lo > 0)
+        if (__any_sync(~0u, (__float_as_uint(v0) - lo_bits < band_bits) |
+                                (__float_as_uint(v1) - lo_bits < band_bits))) {
+            // rare: band points, exact FP64 decides
+            const u32 h0 = __ballot_sync(~0u, v0 < hi_thr);
+            const u32 h1 = __ballot_sync(~0u, v1 < hi_thr);
             if (h0 ^ in0) in0 = band_fix<SHAPE>(in0, h0 ^ in0, S, b, lane, idx, px, py, pz, r, r2);
             if (h1 ^ in1) in1 = band_fix<SHAPE>(in1, h1 ^ in1, S, b + 1, lane, idx, px, py, pz, r, r2);
         }
@@ -95,10 +105,14 @@ __device__ __forceinline__ void process_buffer(PtShared& S, u32 fill, u32 qmask,
             if ((in0 >> lane) & 1u) out_tile[c0 + __popc(in0 & lt)] = idx;
             if ((in1 >> lane) & 1u) out_tile[c1 + __popc(in1 & lt)] = idx;
             mine += lane == b ? __popc(in0) : (lane == b + 1 ? __popc(in1) : 0u);
-        } else {
-            // lane L keeps query L's membership mask of this buffer (count + record)
-            mymask = lane == b ? in0 : (lane == b + 1 ? in1 : mymask);
+        } else if (lane == 0) {
+            // query L's membership mask of this buffer (count + record)
+            *reinterpret_cast<uint2*>(&S.msk[b]) = make_uint2(in0, in1);
         }
+    }
+    if (!FILL) {
+        __syncwarp();
+        mymask = S.msk[lane];
     }
 }
 
