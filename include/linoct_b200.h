@@ -179,6 +179,10 @@ int lo_radius(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int
  * centres, search.hpp:61-64): queries_host is AoS f64, m*3. */
 int lo_radius_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int shape,
                      double radius, const double* queries_host, uint64_t m, lo_csr** out);
+/* neighbours_struct(tree, coded, SearchKernel) at explicit centres (search.hpp:75-78): a
+ * Struct result (see lo_csr_struct_download), with Struct fingerprints. */
+int lo_radius_struct_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int shape,
+                            double radius, const double* queries_host, uint64_t m, lo_csr** out);
 /* Full mode restricted to the contiguous centre range [begin, end) (a shard of the
  * SFC-ordered queries); row r is centre begin + r, indices stay global. */
 int lo_radius_range(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int method,
@@ -189,6 +193,15 @@ int lo_csr_info_get(const lo_csr* csr, lo_csr_info* out);
 int lo_csr_download(lo_context* ctx, const lo_csr* csr, uint32_t* counts_host,
                     uint64_t* fingerprints_host, uint64_t* offsets_host, uint32_t* indices_host);
 int lo_csr_device_ptrs(const lo_csr* csr, const uint64_t** offsets, const uint32_t** indices);
+/* RadiusMethod::Struct results (neighbours_struct, search.cpp:76-135; RangedResult,
+ * search.hpp:18-56): per row the coalesced contained ranges and the singles, each as a CSR
+ * (u64 row offsets; ranges as (begin, end) u32 pairs).  Fingerprints of a Struct result hash
+ * ranges, a separator, then singles (search.cpp:325-336); counts/offsets/indices above are
+ * the expanded rows (RangedResult::expand).  LO_INVALID_ARGUMENT for a Lin/Prune result. */
+int lo_csr_struct_info(const lo_csr* csr, uint64_t* total_ranges, uint64_t* total_singles);
+int lo_csr_struct_download(lo_context* ctx, const lo_csr* csr, uint64_t* range_offsets_host,
+                           uint32_t* ranges_host, uint64_t* single_offsets_host,
+                           uint32_t* singles_host);
 int lo_csr_destroy(lo_csr* csr);
 
 /* ---- kNN (search.cpp:158-259, :369-388) --------------------------------------------- */

@@ -667,3 +667,136 @@ uint64_t or_fnv_knn_row(const uint32_t* idx, const double* dist, uint64_t count)
     }
     return h;
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* neighbours_struct (search.cpp:76-135): pruned traversal over the octant boxes          */
+
+/* kernel_octant_relation (geometry.hpp:197-231): 0 Contains, 1 Disjoint, 2 Intersects */
+static int octant_relation(int shape, const double c[3], double r, double r2, const double b[6]) {
+    double nr[3], fr[3];
+    for (int a = 0; a < 3; ++a) {
+        double nn = b[a] - c[a];
+        if (c[a] - b[3 + a] > nn) nn = c[a] - b[3 + a];
+        if (0.0 > nn) nn = 0.0;
+        const double f1 = c[a] - b[a], f2 = b[3 + a] - c[a];
+        nr[a] = nn;
+        fr[a] = f1 < f2 ? f2 : f1;  /* std::max(a, b) returns a unless a < b */
+    }
+    double nm, fm, lim;
+    switch (shape) {
+        case 0:
+            nm = nr[0] * nr[0] + nr[1] * nr[1] + nr[2] * nr[2];
+            fm = fr[0] * fr[0] + fr[1] * fr[1] + fr[2] * fr[2];
+            lim = r2;
+            break;
+        case 1:
+            nm = nr[0] * nr[0] + nr[1] * nr[1];
+            fm = fr[0] * fr[0] + fr[1] * fr[1];
+            lim = r2;
+            break;
+        case 2:
+            nm = nr[0]; if (nm < nr[1]) nm = nr[1]; if (nm < nr[2]) nm = nr[2];
+            fm = fr[0]; if (fm < fr[1]) fm = fr[1]; if (fm < fr[2]) fm = fr[2];
+            lim = r;
+            break;
+        default:
+            nm = nr[0]; if (nm < nr[1]) nm = nr[1];
+            fm = fr[0]; if (fm < fr[1]) fm = fr[1];
+            lim = r;
+            break;
+    }
+    if (fm < lim) return 0;
+    if (nm >= lim) return 1;
+    return 2;
+}
+
+int64_t or_radius_struct(const double* xyz, const uint64_t* boundaries, const uint32_t* offsets,
+                         const or_node* nodes, int32_t root, const double disc_box[6], int level,
+                         int curve, const double c[3], double r, int shape, uint32_t* ranges,
+                         uint64_t cap_ranges, uint32_t* singles, uint64_t cap_singles,
+                         uint64_t* n_ranges, uint64_t* n_singles) {
+    const double r2 = r * r;
+    uint64_t nr = 0, ns = 0, count = 0;
+    int32_t stack[8 * 64 + 8];
+    int sp = 0;
+    stack[sp++] = root;  /* reorder rejects empty clouds, so the tree has points */
+    while (sp > 0) {
+        const int32_t ref = stack[--sp];
+        uint64_t prefix;
+        int depth;
+        uint32_t b, e;
+        if (ref < 0) {
+            const uint32_t id = (uint32_t)~ref;
+            prefix = boundaries[id];
+            const uint64_t span = boundaries[id + 1] - boundaries[id];
+            int lg = 0;
+            while ((1ULL << (3 * lg)) < span) ++lg;
+            depth = level - lg;
+            b = offsets[id];
+            e = offsets[id + 1];
+        } else {
+            prefix = nodes[ref].prefix;
+            depth = nodes[ref].depth;
+            b = nodes[ref].begin;
+            e = nodes[ref].end;
+        }
+        /* prefix_to_octant_bounds (sfc.cpp:129-141) == the Frame's CurveStepper coordinates */
+        uint32_t cell[3];
+        sfc_decode(curve, prefix, level, cell);
+        const int sh = level - depth;
+        double box[6];
+        or_octant_bounds(disc_box, sh >= 32 ? 0 : cell[0] >> sh, sh >= 32 ? 0 : cell[1] >> sh,
+                         sh >= 32 ? 0 : cell[2] >> sh, depth, box);
+        const int rel = octant_relation(shape, c, r, r2, box);
+        if (rel == 1) continue;
+        if (rel == 0) {  /* search.cpp:124-129: adjacent ranges coalesce */
+            if (nr > 0 && ranges[2 * (nr - 1) + 1] == b) {
+                ranges[2 * (nr - 1) + 1] = e;
+            } else {
+                if (nr >= cap_ranges) return -1;
+                ranges[2 * nr] = b;
+                ranges[2 * nr + 1] = e;
+                ++nr;
+            }
+            count += e - b;
+            continue;
+        }
+        if (ref < 0) {
+            for (uint32_t i = b; i < e; ++i)
+                if (contains(shape, c, r, r2, xyz + 3 * (uint64_t)i)) {
+                    if (ns >= cap_singles) return -1;
+                    singles[ns++] = i;
+                    ++count;
+                }
+        } else {
+            for (int ch = 7; ch >= 0; --ch) {  /* push_children (search.cpp:30-41) */
+                const int32_t cr = nodes[ref].children[ch];
+                uint32_t cb, ce;
+                if (cr < 0) {
+                    cb = offsets[~cr];
+                    ce = offsets[~cr + 1];
+                } else {
+                    cb = nodes[cr].begin;
+                    ce = nodes[cr].end;
+                }
+                if (cb == ce) continue;
+                if (sp >= (int)(sizeof stack / sizeof stack[0])) return -1;
+                stack[sp++] = cr;
+            }
+        }
+    }
+    *n_ranges = nr;
+    *n_singles = ns;
+    return (int64_t)count;
+}
+
+/* search.cpp:325-336: ranges as (begin << 32 | end), a separator, then the singles */
+uint64_t or_fnv_struct_row(const uint32_t* ranges, uint64_t n_ranges, const uint32_t* singles,
+                           uint64_t n_singles) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (uint64_t j = 0; j < n_ranges; ++j)
+        h = or_fnv_u64(h, ((uint64_t)ranges[2 * j] << 32) | ranges[2 * j + 1]);
+    h = or_fnv_u64(h, 0xffffffffffffffffULL);
+    for (uint64_t j = 0; j < n_singles; ++j) h = or_fnv_u64(h, singles[j]);
+    return h;
+}

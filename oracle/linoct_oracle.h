@@ -99,6 +99,17 @@ uint32_t or_knn_brute(const double* xyz, uint64_t n, const double c[3], uint32_t
 uint64_t or_fnv_u64(uint64_t h, uint64_t v);
 uint64_t or_fnv_radius_row(const uint32_t* idx, uint64_t count);
 uint64_t or_fnv_knn_row(const uint32_t* idx, const double* dist, uint64_t count);
+/* neighbours_struct (search.cpp:76-135) for one centre over the tree arrays: ranges as
+ * (begin, end) pairs, coalesced when adjacent; singles ascending.  Returns the member
+ * count (RangedResult::count), or -1 when a capacity is exceeded. */
+int64_t or_radius_struct(const double* xyz, const uint64_t* boundaries, const uint32_t* offsets,
+                         const or_node* nodes, int32_t root, const double disc_box[6], int level,
+                         int curve, const double c[3], double r, int shape, uint32_t* ranges,
+                         uint64_t cap_ranges, uint32_t* singles, uint64_t cap_singles,
+                         uint64_t* n_ranges, uint64_t* n_singles);
+/* search.cpp:325-336: the Struct row digest */
+uint64_t or_fnv_struct_row(const uint32_t* ranges, uint64_t n_ranges, const uint32_t* singles,
+                           uint64_t n_singles);
 
 #ifdef __cplusplus
 }

@@ -75,6 +75,11 @@ class Oracle:
         L.or_fnv_knn_row.argtypes = [P, P, u64]
         L.or_fnv_knn_row.restype = u64
         L.or_sample_indices.argtypes = [u32, u32, u64, P]
+        L.or_radius_struct.argtypes = [P, P, P, P, C.c_int32, P, C.c_int, C.c_int, P, f64, C.c_int,
+                                       P, u64, P, u64, P, P]
+        L.or_radius_struct.restype = i64
+        L.or_fnv_struct_row.argtypes = [P, u64, P, u64]
+        L.or_fnv_struct_row.restype = u64
 
     # generators -------------------------------------------------------------------------
     def gen_uniform(self, n, seed, extent=100.0):
@@ -187,6 +192,30 @@ class Oracle:
         dist = np.empty(take, np.float64)
         self.L.or_knn_brute(_ptr(xyz), len(xyz), _ptr(c), k, _ptr(idx), _ptr(dist))
         return idx, dist
+
+    def radius_struct(self, xs, b, o, nodes, root, disc_box, curve, c, r, shape=0, level=21):
+        """neighbours_struct restated over the oracle's own tree arrays (sorted cloud xs):
+        (count, ranges (k, 2) u32, singles u32)."""
+        xs = np.ascontiguousarray(xs, np.float64)
+        c = np.ascontiguousarray(c, np.float64)
+        box = np.ascontiguousarray(disc_box, np.float64)
+        cap_r, cap_s = max(1, len(xs)), max(1, len(xs))
+        ranges = np.empty((cap_r, 2), np.uint32)
+        singles = np.empty(cap_s, np.uint32)
+        nr = np.zeros(1, np.uint64)
+        ns = np.zeros(1, np.uint64)
+        nodes = np.ascontiguousarray(nodes) if len(nodes) else np.zeros(1, NODE_DTYPE)
+        cnt = self.L.or_radius_struct(_ptr(xs), _ptr(b), _ptr(o), _ptr(nodes), root, _ptr(box), level,
+                                      curve, _ptr(c), r, shape, _ptr(ranges), cap_r, _ptr(singles),
+                                      cap_s, _ptr(nr), _ptr(ns))
+        if cnt < 0:
+            raise ValueError("radius_struct: capacity exceeded")
+        return int(cnt), ranges[: int(nr[0])].copy(), singles[: int(ns[0])].copy()
+
+    def fnv_struct(self, ranges, singles):
+        ranges = np.ascontiguousarray(ranges, np.uint32)
+        singles = np.ascontiguousarray(singles, np.uint32)
+        return self.L.or_fnv_struct_row(_ptr(ranges), len(ranges), _ptr(singles), len(singles))
 
     def fnv_radius(self, idx):
         idx = np.ascontiguousarray(idx, np.uint32)
@@ -307,6 +336,21 @@ class RefPipeline:
         self.ref.L.ref_radius_point(self.h, shape, _ptr(c), r, _ptr(out), cnt)
         return out
 
+    def radius_struct_point(self, c, r, shape=0):
+        """neighbours_struct at centre c: (count, ranges (k, 2) u32, singles u32)."""
+        c = np.ascontiguousarray(c, np.float64)
+        nr = np.zeros(1, np.uint64)
+        ns = np.zeros(1, np.uint64)
+        L = self.ref.L
+        cnt = L.ref_radius_struct_point(self.h, shape, _ptr(c), r, None, 0, None, 0, _ptr(nr), _ptr(ns))
+        if cnt < 0:
+            raise ValueError(L.ref_last_error().decode())
+        ranges = np.empty((int(nr[0]), 2), np.uint32)
+        singles = np.empty(int(ns[0]), np.uint32)
+        L.ref_radius_struct_point(self.h, shape, _ptr(c), r, _ptr(ranges), len(ranges), _ptr(singles),
+                                  len(singles), _ptr(nr), _ptr(ns))
+        return int(cnt), ranges, singles
+
     def radius_range(self, r, begin, end, shape=0, method=1, threads=None, digests=True):
         """neighbours_lin over the sorted centres [begin, end); returns (wall s, counts, fps)."""
         m = end - begin
@@ -369,6 +413,8 @@ class Ref:
         L.ref_knn_point.argtypes = [P, P, u32, P, P, P]
         L.ref_radius_point.argtypes = [P, C.c_int, P, f64, P, u64]
         L.ref_radius_point.restype = i64
+        L.ref_radius_struct_point.argtypes = [P, C.c_int, P, f64, P, u64, P, u64, P, P]
+        L.ref_radius_struct_point.restype = i64
         L.ref_locality.argtypes = [P, u32, C.c_int, C.c_int, P, P, u64]
         L.ref_locality.restype = i64
         L.ref_radius_range.argtypes = [P, C.c_int, C.c_int, f64, u64, u64, C.c_int, P, P]

@@ -309,6 +309,31 @@ std::int64_t ref_radius_point(void* h, int shape, const double* c, double r, std
     return static_cast<std::int64_t>(v.size());
 }
 
+// neighbours_struct at an arbitrary centre (search.hpp:75-78): ranges as (begin, end) pairs
+// and the singles; returns the member count, -1 on error.  Outputs are written only when
+// they fit the capacities; *n_ranges / *n_singles always receive the sizes.
+std::int64_t ref_radius_struct_point(void* h, int shape, const double* c, double r,
+                                     std::uint32_t* ranges, std::uint64_t cap_ranges,
+                                     std::uint32_t* singles, std::uint64_t cap_singles,
+                                     std::uint64_t* n_ranges, std::uint64_t* n_singles) {
+    auto* p = static_cast<Pipeline*>(h);
+    RangedResult rr;
+    const int rc = guarded([&] {
+        rr = neighbours_struct(*p->tree, p->coded,
+                               SearchKernel(static_cast<KernelShape>(shape), {c[0], c[1], c[2]}, r));
+    });
+    if (rc != 0) return -1;
+    *n_ranges = rr.ranges.size();
+    *n_singles = rr.singles.size();
+    if (rr.ranges.size() <= cap_ranges)
+        for (std::size_t j = 0; j < rr.ranges.size(); ++j) {
+            ranges[2 * j] = rr.ranges[j].first;
+            ranges[2 * j + 1] = rr.ranges[j].second;
+        }
+    if (rr.singles.size() <= cap_singles) std::copy(rr.singles.begin(), rr.singles.end(), singles);
+    return static_cast<std::int64_t>(rr.count());
+}
+
 // kNN locality histogram (locality.cpp:91-97), flattened to (d, count) pairs.
 std::int64_t ref_locality(void* h, std::uint32_t k, int threads, int use_perm_map,
                           std::uint32_t* bins_d, std::uint64_t* bins_c, std::uint64_t cap) {

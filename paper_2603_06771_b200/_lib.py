@@ -78,6 +78,9 @@ SIGNATURES = {
     "lo_csr_download": (cint, [P, P, P, P, P, P]),
     "lo_csr_device_ptrs": (cint, [P, PP, PP]),
     "lo_csr_destroy": (cint, [P]),
+    "lo_csr_struct_info": (cint, [P, P, P]),
+    "lo_csr_struct_download": (cint, [P, P, P, P, P, P]),
+    "lo_radius_struct_points": (cint, [P, P, P, cint, f64, P, u64, PP]),
     "lo_knn": (cint, [P, P, P, u32, P, u64, cint, PP]),
     "lo_knn_points": (cint, [P, P, P, u32, P, u64, PP]),
     "lo_knn_range": (cint, [P, P, P, u32, u64, u64, cint, PP]),

@@ -131,12 +131,16 @@ struct lo_octree {
     lo_internal_node* nodes = nullptr;  // [internal]
     lo::TNode* tn = nullptr;            // [tnodes]
     lo::TNodeF* tf = nullptr;           // [tnodes] FP32 shadow (built lazily for replicas)
+    double* rb = nullptr;               // [tnodes*6] padded octant boxes (Struct; built lazily)
     int max_depth = 0;
 };
 
 namespace lo {
 // Lazily (re)build the FP32 shadows (after a broadcast the replicas only hold the exact data).
 void ensure_float_shadows(lo_context* ctx, const lo_coded* coded, const lo_octree* tree);
+// Lazily build the reference's padded octant box of every traversal node (octant_bounds,
+// sfc.cpp:110-127), which decides neighbours_struct's Contains / Disjoint (search.cpp:92-96).
+void ensure_ref_boxes(lo_context* ctx, const lo_coded* coded, const lo_octree* tree);
 }  // namespace lo
 
 struct lo_csr {
@@ -148,7 +152,25 @@ struct lo_csr {
     lo::u32* indices = nullptr;   // [total]
     lo::u32* counts = nullptr;    // [rows]
     lo::u64* fps = nullptr;       // [rows] or null
+    // RadiusMethod::Struct (RangedResult, search.hpp:18-56): per row the coalesced contained
+    // ranges (begin, end) and the individually tested singles; `indices` is the expansion,
+    // materialised on demand.
+    bool is_struct = false;
+    lo::u64 total_ranges = 0, total_singles = 0;
+    lo::u64* range_offsets = nullptr;   // [rows+1]
+    lo::u32* ranges = nullptr;          // [2*total_ranges]
+    lo::u64* single_offsets = nullptr;  // [rows+1]
+    lo::u32* singles = nullptr;         // [total_singles]
 };
+
+namespace lo {
+struct Queries;
+// radius_struct.cu: RadiusMethod::Struct batch, the on-demand expansion, buffer release.
+lo_csr* radius_struct_search(lo_context* ctx, const lo_octree* t, const lo_coded* c, int shape,
+                             double r, const Queries& q, bool fingerprint);
+void ensure_expanded(lo_context* ctx, lo_csr* csr);
+void free_csr_buffers(lo_context* ctx, lo_csr* csr);
+}  // namespace lo
 
 struct lo_knn_result {
     lo_context* ctx = nullptr;

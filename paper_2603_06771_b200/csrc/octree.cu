@@ -286,6 +286,32 @@ struct BoundsParams {
 __device__ __forceinline__ double pad_down(double v) { return dbl_from_order_key(dbl_order_key(v) - 2); }
 __device__ __forceinline__ double pad_up(double v) { return dbl_from_order_key(dbl_order_key(v) + 2); }
 
+// octant_bounds (sfc.cpp:110-127) of the block at `depth` starting at cell code `prefix`
+// (prefix_to_octant_bounds, sfc.cpp:129-141): decode the top `depth` digits, scale, pad.
+__device__ void octant_box(u64 prefix, int depth, const BoundsParams& p, double* o) {
+    if (depth == 0) {
+        for (int a = 0; a < 6; ++a) o[a] = p.box[a];
+        return;
+    }
+    const u64 top = prefix >> (3 * (p.level - depth));
+    u32 h[3] = {0, 0, 0}, s = 0;
+    for (int d = depth - 1; d >= 0; --d) {
+        const u32 e = p.dec[s * 8 + ((top >> (3 * d)) & 7u)];
+        h[0] = h[0] << 1 | ((e >> 2) & 1u);
+        h[1] = h[1] << 1 | ((e >> 1) & 1u);
+        h[2] = h[2] << 1 | (e & 1u);
+        s = e >> 3;
+    }
+    const double inv = ldexp(1.0, -depth);
+    for (int a = 0; a < 3; ++a) {
+        const double side = (p.box[3 + a] - p.box[a]) * inv;
+        const double lo = p.box[a] + static_cast<double>(h[a]) * side;
+        const double hi = lo + side;
+        o[a] = pad_down(lo);
+        o[3 + a] = pad_up(hi);
+    }
+}
+
 __global__ void node_bounds_kernel(const i32* __restrict__ refs, u64 count,
                                    const lo_internal_node* __restrict__ nodes,
                                    const u64* __restrict__ bounds, BoundsParams p,
@@ -304,29 +330,61 @@ __global__ void node_bounds_kernel(const i32* __restrict__ refs, u64 count,
             prefix = nodes[ref].prefix;
             depth = nodes[ref].depth;
         }
-        double* o = out + 6 * r;
-        if (depth == 0) {
-            for (int a = 0; a < 6; ++a) o[a] = p.box[a];
-            continue;
-        }
-        const u64 top = prefix >> (3 * (p.level - depth));
-        u32 h[3] = {0, 0, 0}, s = 0;
-        for (int d = depth - 1; d >= 0; --d) {
-            const u32 e = p.dec[s * 8 + ((top >> (3 * d)) & 7u)];
-            h[0] = h[0] << 1 | ((e >> 2) & 1u);
-            h[1] = h[1] << 1 | ((e >> 1) & 1u);
-            h[2] = h[2] << 1 | (e & 1u);
-            s = e >> 3;
-        }
-        const double inv = ldexp(1.0, -depth);
-        for (int a = 0; a < 3; ++a) {
-            const double side = (p.box[3 + a] - p.box[a]) * inv;
-            const double lo = p.box[a] + static_cast<double>(h[a]) * side;
-            const double hi = lo + side;
-            o[a] = pad_down(lo);
-            o[3 + a] = pad_up(hi);
-        }
+        octant_box(prefix, depth, p, out + 6 * r);
     }
+}
+
+// Depth of every traversal node, one level per launch (children are one level below).
+__global__ void tnode_depth_step(const TNode* __restrict__ tn, u64 count, u8* __restrict__ depth,
+                                 int d) {
+    for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < count;
+         t += (u64)gridDim.x * blockDim.x) {
+        if (depth[t] != d) continue;
+        const u32 c0 = tn[t].child0, nc = tn[t].nchild;
+        for (u32 j = 0; j < nc; ++j) depth[c0 + j] = static_cast<u8>(d + 1);
+    }
+}
+
+// Padded octant box of every traversal node: the block at its depth holding its first point.
+__global__ void tnode_ref_boxes(const TNode* __restrict__ tn, const u8* __restrict__ depth, u64 count,
+                                const u64* __restrict__ codes, BoundsParams p, double* __restrict__ rb) {
+    for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < count;
+         t += (u64)gridDim.x * blockDim.x) {
+        const int d = depth[t];
+        const u64 code = codes[tn[t].begin];
+        const u64 prefix = d == 0 ? 0ull : code & ~((1ull << (3 * (p.level - d))) - 1ull);
+        octant_box(prefix, d, p, rb + 6 * t);
+    }
+}
+
+void ensure_ref_boxes(lo_context* ctx, const lo_coded* coded, const lo_octree* tree) {
+    auto* t = const_cast<lo_octree*>(tree);
+    if (t->rb) return;
+    const u64 T = t->tnodes;
+    u8* depth = dalloc_t<u8>(ctx, T);
+    double* rb = nullptr;
+    try {
+        rb = dalloc_t<double>(ctx, 6 * T);
+        LO_CUDA(cudaMemsetAsync(depth, 0xff, T, ctx->stream));
+        LO_CUDA(cudaMemsetAsync(depth, 0, 1, ctx->stream));
+        const int g = static_cast<int>(std::max<u64>(1, std::min<u64>((T + 255) / 256, ctx->sm_count * 16ull)));
+        for (int d = 0; d < t->level; ++d) {
+            tnode_depth_step<<<g, 256, 0, ctx->stream>>>(t->tn, T, depth, d);
+            LO_CHECK_LAUNCH();
+        }
+        BoundsParams p;
+        std::memcpy(p.box, t->disc_box, sizeof p.box);
+        p.level = t->level;
+        std::memcpy(p.dec, curve_tables(t->curve).dec, sizeof p.dec);
+        tnode_ref_boxes<<<g, 256, 0, ctx->stream>>>(t->tn, depth, T, coded->codes, p, rb);
+        LO_CHECK_LAUNCH();
+    } catch (...) {
+        dfree(ctx, depth);
+        dfree(ctx, rb);
+        throw;
+    }
+    dfree(ctx, depth);
+    t->rb = rb;
 }
 
 __global__ void check_sorted(const u64* __restrict__ codes, u64 n, u64 full, u32* __restrict__ flags) {
@@ -604,6 +662,7 @@ int lo_octree_destroy(lo_octree* t) {
         dfree(ctx, t->nodes);
         dfree(ctx, t->tn);
         dfree(ctx, t->tf);
+        dfree(ctx, t->rb);
         delete t;
     });
 }

@@ -357,7 +357,9 @@ int lo_radius(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int
         u32* cidx = upload_centres(ctx, centres_host, m, coded->n);
         Queries q{coded->x, coded->y, coded->z, cidx, rows, coded->pf, coded->bmax};
         try {
-            *out = radius_search(ctx, tree, coded, shape, radius, q, fingerprint != 0);
+            *out = method == LO_METHOD_STRUCT
+                       ? radius_struct_search(ctx, tree, coded, shape, radius, q, fingerprint != 0)
+                       : radius_search(ctx, tree, coded, shape, radius, q, fingerprint != 0);
         } catch (...) {
             dfree(ctx, cidx);
             throw;
@@ -385,6 +387,24 @@ int lo_radius_points(lo_context* ctx, const lo_octree* tree, const lo_coded* cod
     });
 }
 
+int lo_radius_struct_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int shape,
+                            double radius, const double* queries_host, uint64_t m, lo_csr** out) {
+    return api([&] {
+        require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
+        double *x = nullptr, *y = nullptr, *z = nullptr, bmax = 0.0;
+        float4* f = nullptr;
+        if (m) upload_points(ctx, coded, queries_host, m, &x, &y, &z, &f, &bmax);
+        Queries q{x, y, z, nullptr, m, f, bmax};
+        try {
+            *out = radius_struct_search(ctx, tree, coded, shape, radius, q, true);
+        } catch (...) {
+            dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f);
+            throw;
+        }
+        dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f);
+    });
+}
+
 int lo_radius_range(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int method,
                     int shape, double radius, uint64_t begin, uint64_t end, int fingerprint,
                     lo_csr** out) {
@@ -396,7 +416,9 @@ int lo_radius_range(lo_context* ctx, const lo_octree* tree, const lo_coded* code
         ensure_float_shadows(ctx, coded, tree);
         Queries q{coded->x + begin, coded->y + begin, coded->z + begin, nullptr, end - begin,
                   coded->pf + begin, coded->bmax};
-        *out = radius_search(ctx, tree, coded, shape, radius, q, fingerprint != 0);
+        *out = method == LO_METHOD_STRUCT
+                   ? radius_struct_search(ctx, tree, coded, shape, radius, q, fingerprint != 0)
+                   : radius_search(ctx, tree, coded, shape, radius, q, fingerprint != 0);
     });
 }
 
@@ -423,28 +445,56 @@ int lo_csr_download(lo_context* ctx, const lo_csr* csr, uint32_t* counts_host,
         if (offsets_host)
             LO_CUDA(cudaMemcpyAsync(offsets_host, csr->offsets, 8 * (csr->rows + 1),
                                     cudaMemcpyDeviceToHost, ctx->stream));
-        if (indices_host && csr->total)
+        if (indices_host && csr->total) {
+            ensure_expanded(ctx, const_cast<lo_csr*>(csr));
             LO_CUDA(cudaMemcpyAsync(indices_host, csr->indices, 4 * csr->total,
                                     cudaMemcpyDeviceToHost, ctx->stream));
+        }
         sync(ctx);
     });
 }
 
 int lo_csr_device_ptrs(const lo_csr* csr, const uint64_t** offsets, const uint32_t** indices) {
     return api([&] {
+        if (indices) ensure_expanded(csr->ctx, const_cast<lo_csr*>(csr));
         if (offsets) *offsets = csr->offsets;
         if (indices) *indices = csr->indices;
+    });
+}
+
+int lo_csr_struct_info(const lo_csr* csr, uint64_t* total_ranges, uint64_t* total_singles) {
+    return api([&] {
+        require(csr && csr->is_struct, LO_INVALID_ARGUMENT, "not a Struct radius result");
+        if (total_ranges) *total_ranges = csr->total_ranges;
+        if (total_singles) *total_singles = csr->total_singles;
+    });
+}
+
+int lo_csr_struct_download(lo_context* ctx, const lo_csr* csr, uint64_t* range_offsets_host,
+                           uint32_t* ranges_host, uint64_t* single_offsets_host,
+                           uint32_t* singles_host) {
+    return api([&] {
+        require(csr && csr->is_struct, LO_INVALID_ARGUMENT, "not a Struct radius result");
+        if (range_offsets_host)
+            LO_CUDA(cudaMemcpyAsync(range_offsets_host, csr->range_offsets, 8 * (csr->rows + 1),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        if (ranges_host && csr->total_ranges)
+            LO_CUDA(cudaMemcpyAsync(ranges_host, csr->ranges, 8 * csr->total_ranges,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        if (single_offsets_host)
+            LO_CUDA(cudaMemcpyAsync(single_offsets_host, csr->single_offsets, 8 * (csr->rows + 1),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        if (singles_host && csr->total_singles)
+            LO_CUDA(cudaMemcpyAsync(singles_host, csr->singles, 4 * csr->total_singles,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
     });
 }
 
 int lo_csr_destroy(lo_csr* csr) {
     return api([&] {
         if (!csr) return;
-        lo_context* ctx = csr->ctx;
-        dfree(ctx, csr->counts);
-        dfree(ctx, csr->offsets);
-        dfree(ctx, csr->indices);
-        dfree(ctx, csr->fps);
+        free_csr_buffers(csr->ctx, csr);
         delete csr;
     });
 }

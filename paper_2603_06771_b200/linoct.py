@@ -450,8 +450,10 @@ def _batch_centers(n: int, options: BatchOptions):
 
 def run_radius_batch(tree: LinearOctree, coded: CodedCloud, method: RadiusMethod,
                      shape: KernelShape, radius: float, options: BatchOptions) -> BatchResult:
-    """search.hpp:135-137.  Lin, Prune and Struct give the same exact sets; fingerprints are
-    the Lin/Prune digests (search.cpp:345-347)."""
+    """search.hpp:135-137.  Lin, Prune and Struct give the same exact sets.  Lin/Prune
+    fingerprints hash the indices (search.cpp:345-347); Struct ones hash the coalesced ranges,
+    a separator and the singles (search.cpp:325-336), and the result carries the ranged rows
+    in `extra` (range_offsets, ranges, single_offsets, singles)."""
     if method == RadiusMethod.Ptr:
         raise InvalidArgument("run_radius_batch: ptr method needs a pointer octree")
     ctx = coded.ctx
@@ -474,10 +476,14 @@ def run_radius_batch(tree: LinearOctree, coded: CodedCloud, method: RadiusMethod
             idx = np.empty(int(info.total), np.uint32)
         check(_lib.lib().lo_csr_download(ctx.h, h, _p(counts), _p(fps) if options.fingerprint else None,
                                          _p(offs), _p(idx)))
+        extra = {}
+        if method == RadiusMethod.Struct:
+            ro, rg, so, sg = _struct_rows(h, ctx, m)
+            extra = dict(range_offsets=ro, ranges=rg, single_offsets=so, singles=sg)
     finally:
         _lib.lib().lo_csr_destroy(h)
     return BatchResult(centers_out, counts, fps, offs, idx, None, wall, float(info.device_ms),
-                       float(info.mean_count))
+                       float(info.mean_count), extra)
 
 
 def run_knn_batch(tree: LinearOctree, coded: CodedCloud, k: int, options: BatchOptions,
@@ -515,6 +521,56 @@ def neighbours_lin(tree: LinearOctree, coded: CodedCloud, kernel: SearchKernel) 
 
 
 neighbours_prune = neighbours_lin
+
+
+@dataclass
+class RangedResult:
+    """search.hpp:18-56: disjoint ascending [begin, end) ranges of wholly contained octants
+    (adjacent ones coalesced) plus the individually tested survivor indices."""
+    ranges: np.ndarray   # (k, 2) u32
+    singles: np.ndarray  # u32, ascending
+
+    def count(self) -> int:
+        return int(len(self.singles) + (self.ranges[:, 1].astype(np.int64) - self.ranges[:, 0]).sum())
+
+    def expand(self) -> np.ndarray:
+        parts = [np.arange(b, e, dtype=np.uint32) for b, e in self.ranges] + [self.singles]
+        out = np.concatenate(parts) if parts else np.zeros(0, np.uint32)
+        return np.sort(out, kind="stable").astype(np.uint32)
+
+
+def _struct_rows(h, ctx, m):
+    """Download a Struct result: per row a RangedResult (CSR of ranges and singles)."""
+    L = _lib.lib()
+    tr, ts = C.c_uint64(), C.c_uint64()
+    check(L.lo_csr_struct_info(h, C.byref(tr), C.byref(ts)))
+    ro = np.empty(m + 1, np.uint64)
+    so = np.empty(m + 1, np.uint64)
+    rg = np.empty((int(tr.value), 2), np.uint32)
+    sg = np.empty(int(ts.value), np.uint32)
+    check(L.lo_csr_struct_download(ctx.h, h, _p(ro), _p(rg), _p(so), _p(sg)))
+    return ro, rg, so, sg
+
+
+def neighbours_struct(tree: LinearOctree, coded: CodedCloud, kernel: SearchKernel) -> RangedResult:
+    """search.hpp:75-78 at one arbitrary centre."""
+    return struct_points(tree, coded, kernel.shape, kernel.radius, np.asarray([kernel.center], float))[0]
+
+
+def struct_points(tree: LinearOctree, coded: CodedCloud, shape: KernelShape, radius: float,
+                  centres_xyz) -> list[RangedResult]:
+    """neighbours_struct at arbitrary centres (one RangedResult per centre)."""
+    if not (radius > 0.0) or not np.isfinite(radius):
+        raise InvalidArgument("kernel radius must be positive and finite")
+    q = np.ascontiguousarray(centres_xyz, np.float64).reshape(-1, 3)
+    h = C.c_void_p()
+    check(_lib.lib().lo_radius_struct_points(coded.ctx.h, tree.h, coded.h, int(shape), float(radius),
+                                             _p(q), len(q), C.byref(h)))
+    try:
+        ro, rg, so, sg = _struct_rows(h, coded.ctx, len(q))
+    finally:
+        _lib.lib().lo_csr_destroy(h)
+    return [RangedResult(rg[ro[i]:ro[i + 1]], sg[so[i]:so[i + 1]]) for i in range(len(q))]
 
 
 def radius_points(tree: LinearOctree, coded: CodedCloud, shape: KernelShape, radius: float,

@@ -74,6 +74,16 @@ def main():
         b, off, nodes = p.tree()
         rad = p.radius(radius, method=1, shape=shape, collect=True, threads=4)
         knn = p.knn(k, collect=True, threads=4)
+        # RadiusMethod::Struct: batch digests (search.cpp:325-336) and, for the first centres,
+        # the RangedResult rows themselves (neighbours_struct, search.cpp:122-135)
+        st = p.radius(radius, method=3, shape=shape, threads=4)
+        s_ro, s_rg, s_so, s_sg = [0], [], [0], []
+        for i in range(min(64, len(xs))):
+            _, rg, sg = p.radius_struct_point(xs[i], radius, shape)
+            s_rg.append(rg.reshape(-1, 2))
+            s_sg.append(sg)
+            s_ro.append(s_ro[-1] + len(rg))
+            s_so.append(s_so[-1] + len(sg))
         raw_codes = r.compute_codes(pts, curve) if level == 21 else np.zeros(0, np.uint64)
         np.savez_compressed(
             os.path.join(OUT, f"{name}.npz"), points=pts, curve=curve, level=level, n_max=n_max,
@@ -81,7 +91,10 @@ def main():
             sorted_points=xs, codes=codes, perm=perm, boundaries=b, offsets=off,
             nodes=nodes.view(np.uint8).reshape(-1, 56), root=p.root, radius_offsets=rad["offsets"],
             radius_indices=rad["indices"], radius_counts=rad["counts"], radius_fps=rad["fps"],
-            knn_idx=knn["idx"], knn_dist=knn["dist"], knn_fps=knn["fps"])
+            knn_idx=knn["idx"], knn_dist=knn["dist"], knn_fps=knn["fps"],
+            struct_counts=st["counts"], struct_fps=st["fps"],
+            struct_range_offsets=np.array(s_ro, np.uint64), struct_ranges=np.concatenate(s_rg).astype(np.uint32),
+            struct_single_offsets=np.array(s_so, np.uint64), struct_singles=np.concatenate(s_sg).astype(np.uint32))
         print(f"{name}: n={len(pts)} leaves={p.leaves} internal={p.internal} "
               f"nbrs={int(rad['counts'].sum())}")
 

@@ -72,6 +72,16 @@ def test_oracle_matches_golden(oracle, name):
         assert np.array_equal(i, g["knn_idx"][q])
         assert np.array_equal(d.view(np.uint64), g["knn_dist"][q].view(np.uint64))
         assert oracle.fnv_knn(i, d) == int(g["knn_fps"][q])
+    # RadiusMethod::Struct: the reference's RangedResult rows and Struct digests
+    ro, rg, so, sg = (g["struct_range_offsets"], g["struct_ranges"], g["struct_single_offsets"],
+                      g["struct_singles"])
+    for q in range(len(ro) - 1):
+        cnt, ranges, singles = oracle.radius_struct(xs, b, o, nodes, root, box, curve, xs[q], r, shape,
+                                                    level)
+        assert np.array_equal(ranges, rg[ro[q]:ro[q + 1]])
+        assert np.array_equal(singles, sg[so[q]:so[q + 1]])
+        assert cnt == int(g["struct_counts"][q]) == int(g["radius_counts"][q])
+        assert oracle.fnv_struct(ranges, singles) == int(g["struct_fps"][q])
 
 
 def test_generators_match_reference(oracle, ref):
