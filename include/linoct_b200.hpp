@@ -363,4 +363,54 @@ inline std::vector<std::uint32_t> neighbours_prune(const LinearOctree& tree, con
     return neighbours_lin(tree, coded, shape, center, radius);
 }
 
+// search.hpp:18-56: contained octants as coalesced [begin, end) ranges plus the singles.
+struct RangedResult {
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> ranges;
+    std::vector<std::uint32_t> singles;
+    std::size_t count() const {
+        std::size_t n = singles.size();
+        for (const auto& [b, e] : ranges) n += e - b;
+        return n;
+    }
+    std::vector<std::uint32_t> expand() const {  // ascending two-pointer merge
+        std::vector<std::uint32_t> out;
+        out.reserve(count());
+        std::size_t r = 0, s = 0;
+        while (r < ranges.size() || s < singles.size()) {
+            if (s == singles.size() || (r < ranges.size() && ranges[r].first < singles[s])) {
+                for (std::uint32_t i = ranges[r].first; i < ranges[r].second; ++i) out.push_back(i);
+                ++r;
+            } else {
+                out.push_back(singles[s++]);
+            }
+        }
+        return out;
+    }
+};
+
+// Ranged rows of a Struct result handle (one RangedResult per row).
+inline std::vector<RangedResult> struct_rows(const Context& ctx, const lo_csr* h, std::size_t rows) {
+    std::uint64_t tr = 0, ts = 0;
+    check(lo_csr_struct_info(h, &tr, &ts));
+    std::vector<std::uint64_t> ro(rows + 1), so(rows + 1);
+    std::vector<std::uint32_t> rg(2 * tr), sg(ts);
+    check(lo_csr_struct_download(ctx.get(), h, ro.data(), rg.data(), so.data(), sg.data()));
+    std::vector<RangedResult> out(rows);
+    for (std::size_t i = 0; i < rows; ++i) {
+        for (std::uint64_t j = ro[i]; j < ro[i + 1]; ++j) out[i].ranges.emplace_back(rg[2 * j], rg[2 * j + 1]);
+        out[i].singles.assign(sg.begin() + so[i], sg.begin() + so[i + 1]);
+    }
+    return out;
+}
+
+// search.hpp:75-78
+inline RangedResult neighbours_struct(const LinearOctree& tree, const CodedCloud& coded,
+                                      KernelShape shape, const Point& center, double radius) {
+    lo_csr* h = nullptr;
+    check(lo_radius_struct_points(coded.context().get(), tree.handle(), coded.handle(),
+                                  static_cast<int>(shape), radius, &center.x, 1, &h));
+    std::unique_ptr<lo_csr, int (*)(lo_csr*)> guard(h, &lo_csr_destroy);
+    return std::move(struct_rows(coded.context(), h, 1)[0]);
+}
+
 }  // namespace linoct::b200

@@ -87,6 +87,16 @@ int main() {
         EXPECT(nb.size() == 1 && nb[0].dist_sq == 0.0);
         auto lin = neighbours_lin(tree, coded, KernelShape::Sphere, {50, 50, 50}, 1e5);
         EXPECT(lin.size() == n);
+        // Struct: ranged rows expand to the Lin rows; a huge kernel contains the root
+        auto st = run_radius_batch(tree, coded, RadiusMethod::Struct, KernelShape::Sphere, 4.0, opt);
+        EXPECT(st.counts == res.counts && st.indices == res.indices);
+        for (std::size_t q = 0; q < n; q += 1499) {
+            auto rr = neighbours_struct(tree, coded, KernelShape::Sphere, cloud[q], 4.0);
+            EXPECT(rr.expand() == res.row(q) && rr.count() == res.counts[q]);
+        }
+        auto all = neighbours_struct(tree, coded, KernelShape::Sphere, {50, 50, 50}, 1e5);
+        EXPECT(all.ranges.size() == 1 && all.ranges[0].first == 0 && all.ranges[0].second == n &&
+               all.singles.empty());
     }
     // reference exception types (reorder.cpp:67, search.cpp:192, linear_octree.cpp:25-33)
     EXPECT(throws<std::invalid_argument>([] { reorder_cloud(PointCloud(), Curve::Morton); }));
