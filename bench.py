@@ -436,17 +436,36 @@ def run_ours(args, cfg):
                 "unit": "GB/s", "frac": achieved / PEAKS["hbm_gbs"], "traffic": None,
                 "peak_source": PEAK_SRC, "algorithmic_bytes_per_launch": dom_bytes,
                 "launch_ms": stages[dom],
-                "note": "radius search is FP64/divergence limited; bytes are algorithmic "
-                        "(24 + 8 + 4*mu per query for the fill kernel, SURVEY.md §8d)"}
+                "note": "bytes are algorithmic (SURVEY.md §8d: 24 + 4 B/query for the count kernel, "
+                        "24 + 8 + 4*mu for the fill); the search kernels are instruction-issue "
+                        "bound (issue_active from ncu), the fill is the HBM-moving kernel"}
+    traffic = {}
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         try:
             tr = json.load(open(traffic_file))
-            if tr.get("kernel_stage") == dom and tr.get("config") == args.config:
-                roofline["traffic"] = tr["dram_bytes_per_launch"]
-                roofline["traffic_source"] = tr.get("source")
-        except (OSError, ValueError, KeyError):
-            pass
+            if tr.get("config") == args.config:
+                traffic = tr.get("stages", {})
+        except (OSError, ValueError):
+            traffic = {}
+    if dom in traffic:
+        roofline["traffic"] = traffic[dom]["dram_bytes_per_launch"]
+        roofline["traffic_source"] = traffic[dom].get("source")
+        if traffic[dom].get("issue_active_pct") is not None:
+            roofline["issue_active"] = traffic[dom]["issue_active_pct"] / 100.0
+    # every stage against the same HBM roofline (algorithmic bytes / device time)
+    per_stage = {}
+    for st, st_ms in stages.items():
+        b = algo_bytes(st)
+        if b and st_ms > 0:
+            rec = {"ms": round(st_ms, 4), "achieved_gbs": round(b / (st_ms * 1e-3) / 1e9, 1),
+                   "frac": round(b / (st_ms * 1e-3) / 1e9 / PEAKS["hbm_gbs"], 4)}
+            if st in traffic:
+                rec["traffic_gbs"] = round(traffic[st]["dram_bytes_per_launch"] / (st_ms * 1e-3) / 1e9, 1)
+                if traffic[st].get("issue_active_pct") is not None:
+                    rec["issue_active"] = round(traffic[st]["issue_active_pct"] / 100.0, 3)
+            per_stage[st] = rec
+    roofline["stages"] = per_stage
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

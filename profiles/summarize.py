@@ -77,7 +77,8 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--launches")
     ap.add_argument("--rep", nargs="*", default=[])
-    ap.add_argument("--stage", help="bench stage name the first --rep kernel corresponds to")
+    ap.add_argument("--stage", nargs="*", default=[],
+                    help="bench stage names the --rep kernels correspond to (same order)")
     ap.add_argument("--config", default="cfg1")
     ap.add_argument("--note", default="")
     a = ap.parse_args()
@@ -87,7 +88,7 @@ def main():
     if a.launches:
         md += ["## Launch list (`--metrics gpu__time_duration.sum --clock-control none`; cold-cache, "
                "serialised: compare shares)", "", launches_table(a.launches), ""]
-    traffic = None
+    traffic = {}
     for i, rep in enumerate(a.rep):
         recs = raw_metrics(rep)
         for rec in recs:
@@ -97,19 +98,27 @@ def main():
                 if m in rec:
                     md.append(f"| {m} | {rec[m][0]} | {rec[m][1]} |")
             md.append("")
-        if i == 0 and recs and a.stage:
+        if i < len(a.stage) and recs:
             r0 = recs[0]
 
             def to_bytes(v):
                 val, unit = float(v[0].replace(",", "")), v[1]
                 return val * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-            traffic = to_bytes(r0["dram__bytes_read.sum"]) + to_bytes(r0["dram__bytes_write.sum"])
+
+            def pct(m):
+                return float(r0[m][0].replace(",", "")) if m in r0 else None
+            traffic[a.stage[i]] = {
+                "dram_bytes_per_launch": to_bytes(r0["dram__bytes_read.sum"]) + to_bytes(r0["dram__bytes_write.sum"]),
+                "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                "warps_active_pct": pct("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                "l2_hit_pct": pct("lts__t_sector_hit_rate.pct"),
+                "kernel": r0["kernel"],
+                "source": f"profiles/{a.tag}_ncu.md ({os.path.basename(rep)}, ncu --set full)"}
     path = os.path.join(HERE, f"{a.tag}_ncu.md")
     open(path, "w").write("\n".join(md) + "\n")
     print("wrote", path)
-    if traffic is not None:
-        tj = {"kernel_stage": a.stage, "config": a.config, "dram_bytes_per_launch": traffic,
-              "source": f"profiles/{a.tag}_ncu.md ({os.path.basename(a.rep[0])}, ncu --set full)"}
+    if traffic:
+        tj = {"config": a.config, "stages": traffic}
         json.dump(tj, open(os.path.join(HERE, "traffic.json"), "w"), indent=1)
         print("traffic", tj)
 
