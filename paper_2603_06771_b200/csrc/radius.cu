@@ -165,8 +165,8 @@ static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
     LO_CHECK_LAUNCH();
 }
 
-// Max records per tile for the fused count -> replay fill (64 buffers x 256 B = 16 KB).
-constexpr u32 kRecCap = 64;
+// Max records per tile for the fused count -> replay fill (128 buffers x 256 B = 32 KB).
+constexpr u32 kRecCap = 128;
 
 static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded* c, int shape,
                              double r, const Queries& q, bool fingerprint) {

@@ -117,7 +117,7 @@ __device__ __forceinline__ void process_buffer(PtShared& S, u32 fill, u32 qmask,
 }
 
 constexpr u32 kRecOverflow = 0xffffffffu;
-constexpr u32 kRecChunk = 512;  // records per warp chunk (128 KB)
+constexpr u32 kRecChunk = 1024;  // records per warp chunk (256 KB)
 
 // Count-pass records, packed: each warp takes chunks of kRecChunk records from a bump
 // allocator and appends its tiles' records contiguously; tile t's records start at record
