@@ -31,7 +31,8 @@ typedef enum {
     LO_LOGIC_ERROR = 3,
     LO_OUT_OF_MEMORY = 4,
     LO_CUDA_ERROR = 5,
-    LO_NO_DEVICE = 6
+    LO_NO_DEVICE = 6,
+    LO_RUNTIME_ERROR = 7  /* std::runtime_error: unreadable / malformed files (io.cpp, linear_octree.cpp:163-189) */
 } lo_status;
 
 /* enum class Curve {Morton, Hilbert} (sfc.hpp:17) */
@@ -167,6 +168,24 @@ int lo_octree_device_ptrs(const lo_octree* tree, void** boundaries, void** offse
                           void** tnodes);
 int lo_octree_create_empty(lo_context* ctx, const lo_coded* coded, const lo_octree_info* info,
                            lo_octree** out);
+
+/* ---- on-disk formats (io.cpp:53-114; linear_octree.cpp:149-190) ---------------------- */
+/* reorder_cloud(read_cloud(path), curve, level) for a PCB1 file: the file is streamed through two
+ * pinned buffers, disk reads overlapping the H2D copies.  Malformed files -> LO_RUNTIME_ERROR
+ * with the reference's messages (bad magic, truncated count/record, non-finite record). */
+int lo_reorder_pcb(lo_context* ctx, const char* path, int curve, int level, lo_coded** out);
+/* write_cloud(coded.cloud, path, BinaryPcb): the reordered cloud as PCB1. */
+int lo_coded_write_pcb(lo_context* ctx, const lo_coded* coded, const char* path);
+/* LinearOctree(LeafArray, Discretizer(disc_box, level), curve, n_max) (linear_octree.cpp:84-105):
+ * validates the leaf array like the reference (invalid_argument texts), then links the internal
+ * nodes on the device.  count = boundaries.size() = offsets.size(); the leaves must index the
+ * points of `coded` (offsets.back() == n, same level and curve). */
+int lo_octree_from_leaves(lo_context* ctx, const lo_coded* coded, const uint64_t* boundaries_host,
+                          const uint32_t* offsets_host, uint64_t count, const double disc_box[6],
+                          int level, int curve, uint32_t n_max, lo_octree** out);
+/* LinearOctree::serialize / deserialize as LOC1 files. */
+int lo_octree_save(lo_context* ctx, const lo_octree* tree, const char* path);
+int lo_octree_load(lo_context* ctx, const lo_coded* coded, const char* path, lo_octree** out);
 
 /* ---- radius search (search.cpp:45-156, :261-351) ------------------------------------ */
 /* run_radius_batch(tree, coded, method, shape, radius, options).  centres_host == NULL is

@@ -336,6 +336,11 @@ class RefPipeline:
         self.ref.L.ref_radius_point(self.h, shape, _ptr(c), r, _ptr(out), cnt)
         return out
 
+    def save_tree(self, path):
+        """LinearOctree::serialize of this pipeline's tree to a LOC1 file."""
+        if self.ref.L.ref_pipeline_save_tree(self.h, os.fsencode(path)) != 0:
+            raise RuntimeError(self.ref.L.ref_last_error().decode())
+
     def radius_struct_point(self, c, r, shape=0):
         """neighbours_struct at centre c: (count, ranges (k, 2) u32, singles u32)."""
         c = np.ascontiguousarray(c, np.float64)
@@ -405,6 +410,12 @@ class Ref:
         L.ref_pipeline_coded.argtypes = [P, P, P, P]
         L.ref_pipeline_tree.argtypes = [P, P, P, P]
         L.ref_build_leaves.argtypes = [P, u64, u32, C.c_int, P, P, u64, P]
+        L.ref_read_cloud.argtypes = [C.c_char_p, P, u64]
+        L.ref_read_cloud.restype = i64
+        L.ref_write_cloud.argtypes = [P, u64, C.c_char_p]
+        L.ref_pipeline_save_tree.argtypes = [P, C.c_char_p]
+        L.ref_link_tree.argtypes = [C.c_char_p, P, P, u64, P, C.c_int, C.c_int, u32, P, P, u64, P, u64,
+                                    P, P, P]
         L.ref_radius.argtypes = [P, C.c_int, C.c_int, f64, C.c_int, u32, u64, C.c_int, C.c_int,
                                  P, P, P, P, P, P]
         L.ref_radius.restype = f64
@@ -471,6 +482,45 @@ class Ref:
         o = np.empty(L + 1, np.uint32)
         self.L.ref_build_leaves(_ptr(codes), len(codes), n_max, level, _ptr(b), _ptr(o), L + 1, _ptr(nl))
         return b, o
+
+    def read_cloud(self, path):
+        """read_cloud(path) (io.cpp:83-89): (n, 3) f64, or raises with the reference's text."""
+        L = self.L
+        n = L.ref_read_cloud(os.fsencode(path), None, 0)
+        if n < 0:
+            raise RuntimeError(L.ref_last_error().decode())
+        out = np.empty((n, 3), np.float64)
+        L.ref_read_cloud(os.fsencode(path), _ptr(out), n)
+        return out
+
+    def write_cloud(self, xyz, path):
+        xyz = np.ascontiguousarray(xyz, np.float64)
+        if self.L.ref_write_cloud(_ptr(xyz), len(xyz), os.fsencode(path)) != 0:
+            raise RuntimeError(self.L.ref_last_error().decode())
+
+    def link_tree(self, path=None, b=None, o=None, box=None, level=21, curve=0, n_max=32):
+        """LinearOctree::deserialize(path), or LinearOctree(LeafArray(b, o), Discretizer(box,
+        level), curve, n_max): (boundaries, offsets, nodes, root).  Errors raise ValueError
+        (invalid_argument) or RuntimeError with the reference's text."""
+        L = self.L
+        leaves, internal, root = np.zeros(1, np.uint64), np.zeros(1, np.uint64), np.zeros(1, np.int32)
+        bb = None if b is None else np.ascontiguousarray(b, np.uint64)
+        oo = None if o is None else np.ascontiguousarray(o, np.uint32)
+        box = None if box is None else np.ascontiguousarray(box, np.float64)
+        cnt = 0 if bb is None else len(bb)
+        pth = None if path is None else os.fsencode(path)
+        args = (pth, _ptr(bb), _ptr(oo), cnt, _ptr(box), level, curve, n_max)
+        rc = L.ref_link_tree(*args, None, None, 0, None, 0, _ptr(leaves), _ptr(internal), _ptr(root))
+        if rc != 0:
+            msg = L.ref_last_error().decode()
+            raise (ValueError if rc == 1 else RuntimeError)(msg)
+        nl, ni = int(leaves[0]), int(internal[0])
+        b_out = np.empty(nl + 1, np.uint64)
+        o_out = np.empty(nl + 1, np.uint32)
+        nodes = np.zeros(ni, NODE_DTYPE)
+        L.ref_link_tree(*args, _ptr(b_out), _ptr(o_out), nl + 1, _ptr(nodes), ni, _ptr(leaves), _ptr(internal),
+                        _ptr(root))
+        return b_out, o_out, nodes, int(root[0])
 
     def pipeline(self, xyz, curve, n_max, level=21, threads=None):
         return RefPipeline(self, xyz, curve, n_max, level, threads)

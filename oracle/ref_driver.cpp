@@ -11,6 +11,9 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <fstream>
+#include <memory>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -351,6 +354,75 @@ std::int64_t ref_locality(void* h, std::uint32_t k, int threads, int use_perm_ma
         }
     }
     return static_cast<std::int64_t>(hist.bins.size());
+}
+
+// ---- on-disk formats (io.cpp, linear_octree.cpp:149-190) ---------------------------------
+// read_cloud(path): returns the count (points written when count <= cap), -1 on error.
+std::int64_t ref_read_cloud(const char* path, double* xyz, std::uint64_t cap) {
+    PointCloud c;
+    const int rc = guarded([&] { c = read_cloud(path); });
+    if (rc != 0) return -1;
+    if (c.size() <= cap)
+        for (std::size_t i = 0; i < c.size(); ++i) {
+            xyz[3 * i] = c[i].x;
+            xyz[3 * i + 1] = c[i].y;
+            xyz[3 * i + 2] = c[i].z;
+        }
+    return static_cast<std::int64_t>(c.size());
+}
+
+int ref_write_cloud(const double* xyz, std::uint64_t n, const char* path) {
+    return guarded([&] {
+        std::vector<Point> pts(n);
+        for (std::uint64_t i = 0; i < n; ++i) pts[i] = {xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]};
+        write_cloud(PointCloud(std::move(pts)), path);
+    });
+}
+
+// LinearOctree::serialize of the pipeline's tree.
+int ref_pipeline_save_tree(void* h, const char* path) {
+    auto* p = static_cast<Pipeline*>(h);
+    return guarded([&] {
+        std::ofstream os(path, std::ios::binary | std::ios::trunc);
+        p->tree->serialize(os);
+        if (!os) throw std::runtime_error("write failed");
+    });
+}
+
+// LinearOctree::deserialize(path) or LinearOctree(LeafArray, Discretizer, curve, n_max) when
+// path is null: leaves / internal nodes / root of the linked tree (sizes always reported;
+// arrays written when they fit).
+int ref_link_tree(const char* path, const std::uint64_t* b_in, const std::uint32_t* o_in,
+                  std::uint64_t count_in, const double* box, int level, int curve, std::uint32_t n_max,
+                  std::uint64_t* b_out, std::uint32_t* o_out, std::uint64_t cap, void* nodes,
+                  std::uint64_t node_cap, std::uint64_t* leaves, std::uint64_t* internal,
+                  std::int32_t* root) {
+    return guarded([&] {
+        std::unique_ptr<LinearOctree> t;
+        if (path) {
+            std::ifstream is(path, std::ios::binary);
+            if (!is) throw std::runtime_error("cannot open");
+            t = std::make_unique<LinearOctree>(LinearOctree::deserialize(is));
+        } else {
+            LeafArray la;
+            la.boundaries.assign(b_in, b_in + count_in);
+            la.offsets.assign(o_in, o_in + count_in);
+            const Discretizer d(Aabb{{box[0], box[1], box[2]}, {box[3], box[4], box[5]}}, level);
+            t = std::make_unique<LinearOctree>(std::move(la), d, curve == 0 ? Curve::Morton : Curve::Hilbert,
+                                               n_max);
+        }
+        const auto& la = t->leaves();
+        *leaves = la.leaf_count();
+        const auto& in = t->internal_nodes();
+        *internal = in.size();
+        *root = t->root();
+        if (la.boundaries.size() <= cap) {
+            std::copy(la.boundaries.begin(), la.boundaries.end(), b_out);
+            std::copy(la.offsets.begin(), la.offsets.end(), o_out);
+        }
+        if (in.size() <= node_cap && !in.empty())
+            std::memcpy(nodes, in.data(), in.size() * sizeof(LinearOctree::InternalNode));
+    });
 }
 
 }  // extern "C"

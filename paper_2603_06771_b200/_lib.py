@@ -16,7 +16,7 @@ P = C.c_void_p
 PP = C.POINTER(C.c_void_p)
 u32, u64, i32, f64, cint = C.c_uint32, C.c_uint64, C.c_int32, C.c_double, C.c_int
 
-OK, INVALID_ARGUMENT, DOMAIN_ERROR, LOGIC_ERROR, OUT_OF_MEMORY, CUDA_ERROR, NO_DEVICE = range(7)
+OK, INVALID_ARGUMENT, DOMAIN_ERROR, LOGIC_ERROR, OUT_OF_MEMORY, CUDA_ERROR, NO_DEVICE, RUNTIME_ERROR = range(8)
 
 
 class CodedInfo(C.Structure):
@@ -79,6 +79,11 @@ SIGNATURES = {
     "lo_csr_device_ptrs": (cint, [P, PP, PP]),
     "lo_csr_destroy": (cint, [P]),
     "lo_csr_struct_info": (cint, [P, P, P]),
+    "lo_reorder_pcb": (cint, [P, C.c_char_p, cint, cint, PP]),
+    "lo_coded_write_pcb": (cint, [P, P, C.c_char_p]),
+    "lo_octree_from_leaves": (cint, [P, P, P, P, u64, P, cint, cint, u32, PP]),
+    "lo_octree_save": (cint, [P, P, C.c_char_p]),
+    "lo_octree_load": (cint, [P, P, C.c_char_p, PP]),
     "lo_csr_struct_download": (cint, [P, P, P, P, P, P]),
     "lo_radius_struct_points": (cint, [P, P, P, cint, f64, P, u64, PP]),
     "lo_knn": (cint, [P, P, P, u32, P, u64, cint, PP]),
@@ -142,7 +147,12 @@ class CudaError(LinoctError, RuntimeError):
     """CUDA failure, out of memory, or no device"""
 
 
-_EXC = {INVALID_ARGUMENT: InvalidArgument, DOMAIN_ERROR: DomainError, LOGIC_ERROR: LogicError}
+class FileFormatError(LinoctError, RuntimeError):
+    """std::runtime_error: unreadable or malformed PCB1 / XYZ / LOC1 files"""
+
+
+_EXC = {INVALID_ARGUMENT: InvalidArgument, DOMAIN_ERROR: DomainError, LOGIC_ERROR: LogicError,
+        RUNTIME_ERROR: FileFormatError}
 
 
 def check(status: int) -> None:

@@ -169,6 +169,12 @@ struct Queries;
 lo_csr* radius_struct_search(lo_context* ctx, const lo_octree* t, const lo_coded* c, int shape,
                              double r, const Queries& q, bool fingerprint);
 void ensure_expanded(lo_context* ctx, lo_csr* csr);
+// reorder.cu: reorder_cloud over a device AoS cloud.
+lo_coded* reorder_device(lo_context* ctx, const double* xyz, u64 n, int curve, int level);
+// octree.cu: LinearOctree(LeafArray, Discretizer, Curve, n_max) over host leaf arrays.
+lo_octree* octree_from_leaves(lo_context* ctx, const lo_coded* coded, const u64* b_host,
+                              const u32* off_host, u64 count, const double disc_box[6], int level,
+                              int curve, u32 n_max);
 void free_csr_buffers(lo_context* ctx, lo_csr* csr);
 }  // namespace lo
 

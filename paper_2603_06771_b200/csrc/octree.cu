@@ -455,12 +455,11 @@ static void validate_codes(lo_context* ctx, const u64* codes, u64 n, int level) 
     require(!(f & 2u), LO_INVALID_ARGUMENT, "build_leaves: code exceeds 8^level");
 }
 
-static lo_octree* octree_build(lo_context* ctx, const lo_coded* coded, u32 n_max) {
-    require(coded != nullptr, LO_INVALID_ARGUMENT, "null coded cloud");
-    require(n_max >= 1, LO_INVALID_ARGUMENT, "build_leaves: n_max must be >= 1");
+// Traversal table, tight boxes and FP32 shadow over a finished LeafBuild; takes ownership of
+// lb's buffers.
+static lo_octree* finish_octree(lo_context* ctx, const lo_coded* coded, LeafBuild& lb, u32 n_max,
+                                int level, int curve, const double disc_box[6]) {
     const u64 n = coded->n;
-    stage_begin(ctx, "build");
-    LeafBuild lb = build_tables(ctx, coded->codes, n, n_max, coded->level);
     auto* t = new lo_octree;
     t->ctx = ctx;
     t->coded = coded;
@@ -469,9 +468,9 @@ static lo_octree* octree_build(lo_context* ctx, const lo_coded* coded, u32 n_max
     t->internal = lb.internal;
     t->root = lb.internal > 0 ? 0 : ~0;
     t->n_max = n_max;
-    t->level = coded->level;
-    t->curve = coded->curve;
-    std::memcpy(t->disc_box, coded->disc_box, sizeof t->disc_box);
+    t->level = level;
+    t->curve = curve;
+    std::memcpy(t->disc_box, disc_box, sizeof t->disc_box);
     t->bounds = lb.bounds;
     t->offsets = lb.offsets;
     t->nodes = lb.nodes;
@@ -500,13 +499,148 @@ static lo_octree* octree_build(lo_context* ctx, const lo_coded* coded, u32 n_max
                                                               coded->z, parent, tid_of, arrivals);
     LO_CHECK_LAUNCH();
     build_float_nodes(ctx, t, coded);
-    stage_end(ctx);
     dfree(ctx, tbase);
     dfree(ctx, parent);
     dfree(ctx, tid_of);
     dfree(ctx, arrivals);
     dfree(ctx, lb.nchild);
+    lb = LeafBuild{};
     sync(ctx);
+    return t;
+}
+
+static lo_octree* octree_build(lo_context* ctx, const lo_coded* coded, u32 n_max) {
+    require(coded != nullptr, LO_INVALID_ARGUMENT, "null coded cloud");
+    require(n_max >= 1, LO_INVALID_ARGUMENT, "build_leaves: n_max must be >= 1");
+    stage_begin(ctx, "build");
+    LeafBuild lb = build_tables(ctx, coded->codes, coded->n, n_max, coded->level);
+    lo_octree* t = finish_octree(ctx, coded, lb, n_max, coded->level, coded->curve, coded->disc_box);
+    stage_end(ctx);
+    return t;
+}
+
+// ---- LinearOctree(LeafArray, Discretizer, Curve, n_max) (linear_octree.cpp:84-137) ------
+// link_range's recursion, without recursion: leaf i starts the internal blocks at the depths d
+// < depth(leaf i) at which its start b[i] is block-aligned, and preorder == (first leaf,
+// depth), so a scan of the per-leaf counts numbers the nodes like link_range does.
+__device__ __forceinline__ int leaf_depth(u64 span, int level) {
+    return level - (__ffsll(static_cast<long long>(span)) - 1) / 3;
+}
+__device__ __forceinline__ int first_open_depth(u64 start, int level) {
+    if (start == 0) return 0;
+    const int tz = (__ffsll(static_cast<long long>(start)) - 1) / 3;  // trailing zero octal digits
+    return tz >= level ? 0 : level - tz;
+}
+
+__global__ void leaf_open_count(const u64* __restrict__ b, u64 leaves, int level, u32* __restrict__ cnt) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < leaves;
+         i += (u64)gridDim.x * blockDim.x) {
+        const int dl = leaf_depth(b[i + 1] - b[i], level);
+        const int d0 = first_open_depth(b[i], level);
+        cnt[i] = dl > d0 ? static_cast<u32>(dl - d0) : 0u;
+    }
+}
+
+// exact-match lower_bound over the boundaries (the tiling guarantees the key is present)
+__device__ __forceinline__ u64 find_boundary(const u64* __restrict__ b, u64 lo, u64 hi, u64 key) {
+    while (lo < hi) {
+        const u64 mid = (lo + hi) >> 1;
+        if (b[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void leaf_link(const u64* __restrict__ b, const u32* __restrict__ off, u64 leaves,
+                          int level, const u32* __restrict__ cnt, const u32* __restrict__ S,
+                          lo_internal_node* __restrict__ nodes, u32* __restrict__ nchild) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < leaves;
+         i += (u64)gridDim.x * blockDim.x) {
+        const u32 c_i = cnt[i];
+        if (!c_i) continue;
+        const u64 s = b[i];
+        const int d0 = first_open_depth(s, level);
+        for (u32 j = 0; j < c_i; ++j) {
+            const int d = d0 + static_cast<int>(j);
+            const u64 blk = 1ull << (3 * (level - d)), sub = blk >> 3;
+            const u64 e_leaf = find_boundary(b, i + 1, leaves + 1, s + blk);
+            lo_internal_node nd;
+            nd.prefix = s;
+            nd.begin = off[i];
+            nd.end = off[e_leaf];
+            nd.depth = static_cast<u8>(d);
+            u8 mask = 0;
+            u64 jl = i;
+            for (int c = 0; c < 8; ++c) {
+                const u64 cs = s + c * sub;
+                jl = find_boundary(b, jl, e_leaf, cs);
+                const u64 ce = find_boundary(b, jl + 1, e_leaf + 1, cs + sub);
+                i32 child;
+                if (ce == jl + 1) {
+                    child = ~static_cast<i32>(jl);  // the child block is one leaf
+                } else {
+                    const int dj0 = first_open_depth(b[jl], level);
+                    child = static_cast<i32>(S[jl] + static_cast<u32>(d + 1 - dj0));
+                }
+                nd.children[c] = child;
+                if (off[ce] != off[jl]) mask |= static_cast<u8>(1u << c);
+            }
+            nd.child_mask = mask;
+            for (int q = 0; q < 6; ++q) nd.pad_[q] = 0;
+            nodes[S[i] + j] = nd;
+            nchild[S[i] + j] = __popc(mask);
+        }
+    }
+}
+
+lo_octree* octree_from_leaves(lo_context* ctx, const lo_coded* coded, const u64* b_host,
+                              const u32* off_host, u64 count, const double disc_box[6], int level,
+                              int curve, u32 n_max) {
+    require(coded != nullptr, LO_INVALID_ARGUMENT, "null coded cloud");
+    // Discretizer ctor (sfc.cpp:99-104)
+    require(level >= 0 && level <= kMaxLevel, LO_INVALID_ARGUMENT, "level out of range");
+    require(disc_box[0] <= disc_box[3] && disc_box[1] <= disc_box[4] && disc_box[2] <= disc_box[5],
+            LO_INVALID_ARGUMENT, "inverted bounding box");
+    // LinearOctree(LeafArray, ...) validation (linear_octree.cpp:88-103)
+    const u64 full = 1ull << (3 * level);
+    require(count >= 2 && b_host[0] == 0 && b_host[count - 1] == full && off_host[0] == 0,
+            LO_INVALID_ARGUMENT, "linear octree: malformed leaf array");
+    for (u64 i = 0; i + 1 < count; ++i) {
+        const u64 span = b_host[i + 1] - b_host[i];
+        const bool aligned_pow8 = b_host[i + 1] > b_host[i] && (span & (span - 1)) == 0 &&
+                                  __builtin_ctzll(span) % 3 == 0 && b_host[i] % span == 0;
+        require(aligned_pow8 && off_host[i] <= off_host[i + 1], LO_INVALID_ARGUMENT,
+                "linear octree: misaligned leaf span at " + std::to_string(i));
+    }
+    // the device tree searches this cloud: its leaves must index exactly its points
+    require(off_host[count - 1] == coded->n && level == coded->level && curve == coded->curve,
+            LO_INVALID_ARGUMENT, "linear octree: leaf array does not match the coded cloud");
+    const u64 L = count - 1;
+    stage_begin(ctx, "build");
+    LeafBuild lb;
+    lb.leaves = L;
+    lb.bounds = dalloc_t<u64>(ctx, count);
+    lb.offsets = dalloc_t<u32>(ctx, count);
+    LO_CUDA(cudaMemcpyAsync(lb.bounds, b_host, 8 * count, cudaMemcpyHostToDevice, ctx->stream));
+    LO_CUDA(cudaMemcpyAsync(lb.offsets, off_host, 4 * count, cudaMemcpyHostToDevice, ctx->stream));
+    u32* cnt = dalloc_t<u32>(ctx, L);
+    u32* S = dalloc_t<u32>(ctx, L + 1);
+    leaf_open_count<<<grid1(ctx, L), 256, 0, ctx->stream>>>(lb.bounds, L, level, cnt);
+    LO_CHECK_LAUNCH();
+    exclusive_scan_u32(ctx, cnt, S, L);
+    const u32 I = read_scalar(ctx, S + L);
+    lb.internal = I;
+    lb.nodes = dalloc_t<lo_internal_node>(ctx, I);
+    lb.nchild = dalloc_t<u32>(ctx, I + 1);
+    if (I > 0) {
+        leaf_link<<<grid1(ctx, L, 128), 128, 0, ctx->stream>>>(lb.bounds, lb.offsets, L, level, cnt, S,
+                                                               lb.nodes, lb.nchild);
+        LO_CHECK_LAUNCH();
+    }
+    dfree(ctx, cnt);
+    dfree(ctx, S);
+    lo_octree* t = finish_octree(ctx, coded, lb, n_max, level, curve, disc_box);
+    stage_end(ctx);
     return t;
 }
 

@@ -467,7 +467,7 @@ static void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, 
     dfree(ctx, vtmp);
 }
 
-static lo_coded* reorder_device(lo_context* ctx, const double* xyz, u64 n, int curve, int level) {
+lo_coded* reorder_device(lo_context* ctx, const double* xyz, u64 n, int curve, int level) {
     require(n > 0, LO_INVALID_ARGUMENT, "reorder_cloud: empty cloud");
     require(n <= 0xffffffffull, LO_INVALID_ARGUMENT,
             "reorder_cloud: cloud exceeds 32-bit index space");

@@ -16,13 +16,16 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
+import re
 import time
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _lib
-from ._lib import CodedInfo, CsrInfo, DomainError, InvalidArgument, LogicError, OctreeInfo, check
+from ._lib import (CodedInfo, CsrInfo, DomainError, FileFormatError, InvalidArgument, LogicError, OctreeInfo,
+                   check)
 
 __all__ = [
     "Curve", "KernelShape", "RadiusMethod", "BatchMode", "BatchOptions", "BatchResult",
@@ -196,6 +199,10 @@ class CodedCloud:
                 pass
             self.h = None
 
+    def write_pcb(self, path: str) -> None:
+        """write_cloud(coded.cloud, path, BinaryPcb): the reordered cloud as PCB1."""
+        check(_lib.lib().lo_coded_write_pcb(self.ctx.h, self.h, os.fsencode(path)))
+
     def _download(self, xyz=False, codes=False, perm=False):
         a = np.empty((self.n, 3)) if xyz else None
         c = np.empty(self.n, np.uint64) if codes else None
@@ -224,6 +231,93 @@ class CodedCloud:
     @property
     def discretizer(self):
         return {"bbox": self.disc_box.copy(), "level": self.level, "scale": self.scale.copy()}
+
+
+class CloudFormat(enum.IntEnum):  # io.hpp:14
+    TextXyz = 0
+    BinaryPcb = 1
+
+
+def format_from_path(path: str) -> CloudFormat:
+    """io.cpp:16-23."""
+    dot = path.rfind(".")
+    ext = "" if dot < 0 else path[dot:]
+    if ext == ".pcb":
+        return CloudFormat.BinaryPcb
+    if ext in (".xyz", ".txt"):
+        return CloudFormat.TextXyz
+    raise InvalidArgument(f"cannot infer cloud format from '{path}' (expected .pcb, .xyz or .txt)")
+
+
+_DECIMAL = re.compile(r"^[+-]?(\d+\.?\d*|\.\d+)([eE][+-]?\d+)?$")
+
+
+def read_cloud(path: str, fmt: CloudFormat | None = None) -> PointCloud:
+    """read_cloud (io.cpp:27-85) on the host: PCB1 or text XYZ, the reference's error texts."""
+    fmt = format_from_path(path) if fmt is None else fmt
+    if fmt == CloudFormat.TextXyz:
+        try:
+            lines = open(path).read().split("\n")
+        except OSError:
+            raise FileFormatError(f"cannot open '{path}'") from None
+        pts = []
+        for no, line in enumerate(lines, 1):
+            t = line.strip(" \t\r")
+            if not t or t.startswith("#"):
+                continue
+            f = t.split()
+            # what `std::istream >> double` accepts: decimal reals only (no inf/nan/hex), and an
+            # out-of-range value is a failed extraction
+            if len(f) != 3 or not all(_DECIMAL.match(x) for x in f):
+                raise FileFormatError(f"{path}:{no}: expected three reals")
+            p = [float(x) for x in f]
+            if not all(np.isfinite(p)):
+                raise FileFormatError(f"{path}:{no}: expected three reals")
+            if not all(np.isfinite(p)):
+                raise FileFormatError(f"{path}:{no}: non-finite coordinate")
+            pts.append(p)
+        return PointCloud(np.array(pts, np.float64).reshape(-1, 3))
+    try:
+        raw = open(path, "rb").read()
+    except OSError:
+        raise FileFormatError(f"cannot open '{path}'") from None
+    if raw[:4] != b"PCB1":
+        raise FileFormatError(f"{path}: bad magic at byte offset 0")
+    if len(raw) < 12:
+        raise FileFormatError(f"{path}: truncated count at byte offset 4")
+    count = int(np.frombuffer(raw, "<u8", 1, 4)[0])
+    have = (len(raw) - 12) // 24
+    if have < count:
+        raise FileFormatError(f"{path}: truncated record at byte offset {12 + 24 * have}")
+    a = np.frombuffer(raw, "<f8", 3 * count, 12).reshape(count, 3).astype(np.float64)
+    bad = ~np.isfinite(a).all(axis=1)
+    if bad.any():
+        raise FileFormatError(f"{path}: non-finite coordinate in record {int(np.argmax(bad))}")
+    return PointCloud(a)
+
+
+def write_cloud(cloud, path: str, fmt: CloudFormat | None = None) -> None:
+    """write_cloud (io.cpp:94-120): PCB1 little-endian, or '%.17g %.17g %.17g' lines."""
+    fmt = format_from_path(path) if fmt is None else fmt
+    pts = _as_points(cloud)
+    try:
+        with open(path, "wb") as f:
+            if fmt == CloudFormat.BinaryPcb:
+                f.write(b"PCB1" + np.uint64(len(pts)).astype("<u8").tobytes())
+                f.write(np.ascontiguousarray(pts, "<f8").tobytes())
+            else:
+                f.write("".join("%.17g %.17g %.17g\n" % tuple(p) for p in pts).encode())
+    except OSError:
+        raise FileFormatError(f"cannot open '{path}' for writing") from None
+
+
+def reorder_pcb(path: str, curve: Curve, level: int = kMaxLevel, ctx: Context | None = None) -> CodedCloud:
+    """reorder_cloud(read_cloud(path), curve, level) for a PCB1 file, streamed from disk to the
+    device through pinned double buffers (disk reads overlap the H2D copies)."""
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    check(_lib.lib().lo_reorder_pcb(ctx.h, os.fsencode(path), int(curve), level, C.byref(h)))
+    return CodedCloud(h, ctx)
 
 
 def compute_codes(cloud, curve: Curve, disc_box=None, level: int = kMaxLevel,
@@ -287,18 +381,47 @@ def build_leaves(codes, n_max: int, level: int = kMaxLevel, threads: int = 1,
 class LinearOctree:
     """linear_octree.hpp:40-118, built on the device from a CodedCloud."""
 
-    def __init__(self, coded: CodedCloud, n_max: int = 128, threads: int = 1):
-        if n_max < 1:
-            raise InvalidArgument("build_leaves: n_max must be >= 1")
+    def __init__(self, coded: CodedCloud, n_max: int = 128, threads: int = 1, _handle=None):
         self.coded = coded
         self.ctx = coded.ctx
-        h = C.c_void_p()
-        check(_lib.lib().lo_octree_build(self.ctx.h, coded.h, n_max, C.byref(h)))
-        self.h = h
+        if _handle is None:
+            if n_max < 1:
+                raise InvalidArgument("build_leaves: n_max must be >= 1")
+            h = C.c_void_p()
+            check(_lib.lib().lo_octree_build(self.ctx.h, coded.h, n_max, C.byref(h)))
+            _handle = h
+        self.h = _handle
         info = OctreeInfo()
         check(_lib.lib().lo_octree_info_get(self.h, C.byref(info)))
         self.info = info
         self._leaves = self._nodes = None
+
+    @classmethod
+    def from_leaves(cls, coded: CodedCloud, leaf_array: "LeafArray", disc_box, level: int, curve: Curve,
+                    n_max: int) -> "LinearOctree":
+        """LinearOctree(LeafArray, Discretizer(disc_box, level), curve, n_max)
+        (linear_octree.cpp:84-105): validated like the reference, linked on the device."""
+        b = np.ascontiguousarray(leaf_array.boundaries, np.uint64)
+        o = np.ascontiguousarray(leaf_array.offsets, np.uint32)
+        if len(b) != len(o):
+            raise InvalidArgument("linear octree: malformed leaf array")
+        box = np.ascontiguousarray(disc_box, np.float64)
+        h = C.c_void_p()
+        check(_lib.lib().lo_octree_from_leaves(coded.ctx.h, coded.h, _p(b), _p(o), len(b), _p(box), int(level),
+                                               int(curve), int(n_max), C.byref(h)))
+        return cls(coded, _handle=h)
+
+    def serialize(self, path: str) -> None:
+        """LinearOctree::serialize (linear_octree.cpp:149-160) to a LOC1 file."""
+        check(_lib.lib().lo_octree_save(self.ctx.h, self.h, os.fsencode(path)))
+
+    @classmethod
+    def deserialize(cls, path: str, coded: CodedCloud) -> "LinearOctree":
+        """LinearOctree::deserialize (linear_octree.cpp:162-190) from a LOC1 file; the tree
+        searches `coded` (its leaves must index exactly those points)."""
+        h = C.c_void_p()
+        check(_lib.lib().lo_octree_load(coded.ctx.h, coded.h, os.fsencode(path), C.byref(h)))
+        return cls(coded, _handle=h)
 
     def __del__(self):
         if getattr(self, "h", None):
