@@ -30,6 +30,7 @@ inline void check(int status) {
         case LO_INVALID_ARGUMENT: throw std::invalid_argument(msg);
         case LO_DOMAIN_ERROR: throw std::domain_error(msg);
         case LO_LOGIC_ERROR: throw std::logic_error(msg);
+        case LO_RUNTIME_ERROR: throw std::runtime_error(msg);
         default: throw std::runtime_error(msg);
     }
 }
@@ -130,6 +131,19 @@ inline CodedCloud reorder_cloud(const PointCloud& cloud, Curve curve, int level 
     return CodedCloud(h, ctx);
 }
 
+// reorder_cloud(read_cloud(path), curve, level) for a PCB1 file, streamed to the device
+// (io.cpp:53-81); malformed files throw std::runtime_error with the reference's texts.
+inline CodedCloud reorder_pcb(const std::string& path, Curve curve, int level = kMaxLevel,
+                              Context& ctx = Context::default_for()) {
+    lo_coded* h = nullptr;
+    check(lo_reorder_pcb(ctx.get(), path.c_str(), static_cast<int>(curve), level, &h));
+    return CodedCloud(h, ctx);
+}
+// write_cloud(coded.cloud, path, BinaryPcb) (io.cpp:94-106)
+inline void write_pcb(const CodedCloud& coded, const std::string& path) {
+    check(lo_coded_write_pcb(coded.context().get(), coded.handle(), path.c_str()));
+}
+
 // reorder.hpp:36
 inline std::vector<std::uint32_t> invert_permutation(const std::vector<std::uint32_t>& perm,
                                                      Context& ctx = Context::default_for()) {
@@ -170,6 +184,26 @@ class LinearOctree {
         h_.reset(h, &lo_octree_destroy);
         check(lo_octree_info_get(h, &info_));
     }
+    // LinearOctree(LeafArray, Discretizer, Curve, n_max) (linear_octree.cpp:84-105); the leaves
+    // must index `coded`'s points, which the device tree searches.
+    LinearOctree(const CodedCloud& coded, const LeafArray& leaf_array, const std::array<double, 6>& disc_box,
+                 int level, Curve curve, std::uint32_t n_max)
+        : ctx_(&coded.context()) {
+        if (leaf_array.boundaries.size() != leaf_array.offsets.size())
+            throw std::invalid_argument("linear octree: malformed leaf array");
+        lo_octree* h = nullptr;
+        check(lo_octree_from_leaves(ctx_->get(), coded.handle(), leaf_array.boundaries.data(),
+                                    leaf_array.offsets.data(), leaf_array.boundaries.size(), disc_box.data(),
+                                    level, static_cast<int>(curve), n_max, &h));
+        adopt(h);
+    }
+    // LinearOctree::serialize / deserialize (linear_octree.cpp:149-190) as LOC1 files.
+    void serialize(const std::string& path) const { check(lo_octree_save(ctx_->get(), h_.get(), path.c_str())); }
+    static LinearOctree deserialize(const std::string& path, const CodedCloud& coded) {
+        lo_octree* h = nullptr;
+        check(lo_octree_load(coded.context().get(), coded.handle(), path.c_str(), &h));
+        return LinearOctree(h, coded.context());
+    }
     lo_octree* handle() const { return h_.get(); }
     static bool is_leaf(NodeRef r) { return r < 0; }
     static std::uint32_t leaf_id(NodeRef r) { return static_cast<std::uint32_t>(~r); }
@@ -202,6 +236,11 @@ class LinearOctree {
     }
 
   private:
+    LinearOctree(lo_octree* h, Context& ctx) : ctx_(&ctx) { adopt(h); }
+    void adopt(lo_octree* h) {
+        h_.reset(h, &lo_octree_destroy);
+        check(lo_octree_info_get(h, &info_));
+    }
     void fetch() const {
         if (fetched_) return;
         leaves_.boundaries.resize(info_.leaves + 1);

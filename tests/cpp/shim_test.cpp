@@ -3,6 +3,7 @@
 // test_linear_octree.cpp).  Built by __graft_entry__.build(); run by tests/test_cpp_shim.py.
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <stdexcept>
 #include <vector>
@@ -94,6 +95,28 @@ int main() {
             auto rr = neighbours_struct(tree, coded, KernelShape::Sphere, cloud[q], 4.0);
             EXPECT(rr.expand() == res.row(q) && rr.count() == res.counts[q]);
         }
+        // LOC1 round trip and the LeafArray constructor give the same tree
+        const std::string loc = "/tmp/lo_shim_test.loc", pcb = "/tmp/lo_shim_test.pcb";
+        tree.serialize(loc);
+        auto loaded = LinearOctree::deserialize(loc, coded);
+        EXPECT(loaded.leaves().boundaries == tree.leaves().boundaries && loaded.root() == tree.root());
+        EXPECT(loaded.internal_nodes().size() == tree.internal_nodes().size());
+        std::array<double, 6> box{};
+        {
+            lo_coded_info ci{};
+            check(lo_coded_info_get(coded.handle(), &ci));
+            std::copy(ci.disc_box, ci.disc_box + 6, box.begin());
+        }
+        LinearOctree relinked(coded, tree.leaves(), box, 21, curve, 32);
+        EXPECT(relinked.internal_nodes().size() == tree.internal_nodes().size() &&
+               std::memcmp(relinked.internal_nodes().data(), tree.internal_nodes().data(),
+                           tree.internal_nodes().size() * sizeof(lo_internal_node)) == 0);
+        write_pcb(coded, pcb);
+        auto again = reorder_pcb(pcb, curve);
+        EXPECT(again.codes() == coded.codes());
+        EXPECT(throws<std::runtime_error>([&] { reorder_pcb("/nonexistent/x.pcb", curve); }));
+        std::remove(loc.c_str());
+        std::remove(pcb.c_str());
         auto all = neighbours_struct(tree, coded, KernelShape::Sphere, {50, 50, 50}, 1e5);
         EXPECT(all.ranges.size() == 1 && all.ranges[0].first == 0 && all.ranges[0].second == n &&
                all.singles.empty());
