@@ -247,6 +247,16 @@ int lo_knn_destroy(lo_knn_result* res);
 int lo_locality_log2(lo_context* ctx, const lo_knn_result* res, const lo_coded* coded,
                      const uint32_t* centres_host, int use_perm, uint64_t* bins33_host);
 
+/* Exact histogram (LocalityHistogram::bins, locality.cpp:41-97): ascending distinct d with
+ * their counts, d = |map(i) - map(j)| over every (centre i, kNN member j) pair of `res`;
+ * index_map_host (n entries) or NULL for identity, centres_host as passed to lo_knn (NULL =
+ * Full).  *nbins is always set; d_host / count_host are written when nbins <= cap, so call
+ * once with cap = 0 to size.  Statistics (mean, stddev, G1, quartiles) are host arithmetic
+ * over these bins in the reference's order (linoct_b200.hpp / linoct.py). */
+int lo_locality_histogram(lo_context* ctx, const lo_knn_result* res, const lo_coded* coded,
+                          const uint32_t* centres_host, const uint32_t* index_map_host,
+                          uint64_t* nbins, uint32_t* d_host, uint64_t* count_host, uint64_t cap);
+
 /* ---- synthetic clouds (host; io.cpp:122-130 and SURVEY.md §8d) ---------------------- */
 int lo_generate_uniform(uint64_t n, uint64_t seed, double extent, double* xyz_host);
 int lo_generate_terrain(uint64_t n, uint64_t seed, double extent_xy, double* xyz_host);

@@ -381,6 +381,19 @@ class RefPipeline:
             raise ValueError(L.ref_last_error().decode())
         return d[:nb].copy(), c[:nb].copy()
 
+    def locality_stats(self, k, use_perm_map=False, sample=0, seed=0, threads=None):
+        """(bins d, bins count, [mean, stddev, G1, Q1, Q2, Q3]) of locality_histogram(_approx)."""
+        L = self.ref.L
+        th = threads or self.threads
+        out = np.zeros(6)
+        nb = L.ref_locality_stats(self.h, k, th, int(use_perm_map), sample, seed, _ptr(out), None, None, 0)
+        if nb < 0:
+            raise ValueError(L.ref_last_error().decode())
+        d = np.empty(nb, np.uint32)
+        c = np.empty(nb, np.uint64)
+        L.ref_locality_stats(self.h, k, th, int(use_perm_map), sample, seed, _ptr(out), _ptr(d), _ptr(c), nb)
+        return d, c, out
+
 
 class Ref:
     """The unmodified reference library (oracle/_ref/libref_linoct.so)."""
@@ -410,6 +423,8 @@ class Ref:
         L.ref_pipeline_coded.argtypes = [P, P, P, P]
         L.ref_pipeline_tree.argtypes = [P, P, P, P]
         L.ref_build_leaves.argtypes = [P, u64, u32, C.c_int, P, P, u64, P]
+        L.ref_locality_stats.argtypes = [P, u32, C.c_int, C.c_int, u32, u64, P, P, P, u64]
+        L.ref_locality_stats.restype = i64
         L.ref_read_cloud.argtypes = [C.c_char_p, P, u64]
         L.ref_read_cloud.restype = i64
         L.ref_write_cloud.argtypes = [P, u64, C.c_char_p]

@@ -356,6 +356,32 @@ std::int64_t ref_locality(void* h, std::uint32_t k, int threads, int use_perm_ma
     return static_cast<std::int64_t>(hist.bins.size());
 }
 
+// locality_histogram(_approx) + its statistics (locality.cpp:13-140): out = {mean, stddev,
+// G1, Q1, Q2, Q3}; sample = 0 -> exact over all centres.  Returns the bin count, -1 on error.
+std::int64_t ref_locality_stats(void* h, std::uint32_t k, int threads, int use_perm_map,
+                                std::uint32_t sample, std::uint64_t seed, double* out,
+                                std::uint32_t* bins_d, std::uint64_t* bins_c, std::uint64_t cap) {
+    auto* p = static_cast<Pipeline*>(h);
+    LocalityHistogram hist;
+    const auto* map = use_perm_map ? &p->coded.permutation : nullptr;
+    const int rc = guarded([&] {
+        hist = sample ? locality_histogram_approx(*p->tree, p->coded, k, sample, seed, threads, map)
+                      : locality_histogram(*p->tree, p->coded, k, threads, map);
+    });
+    if (rc != 0) return -1;
+    const auto q = histogram_quantiles(hist);
+    out[0] = hist.mean();
+    out[1] = hist.stddev();
+    out[2] = fisher_pearson_skewness(hist);
+    out[3] = q[0], out[4] = q[1], out[5] = q[2];
+    if (hist.bins.size() <= cap)
+        for (std::size_t i = 0; i < hist.bins.size(); ++i) {
+            bins_d[i] = hist.bins[i].first;
+            bins_c[i] = hist.bins[i].second;
+        }
+    return static_cast<std::int64_t>(hist.bins.size());
+}
+
 // ---- on-disk formats (io.cpp, linear_octree.cpp:149-190) ---------------------------------
 // read_cloud(path): returns the count (points written when count <= cap), -1 on error.
 std::int64_t ref_read_cloud(const char* path, double* xyz, std::uint64_t cap) {

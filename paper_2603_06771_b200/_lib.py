@@ -80,6 +80,7 @@ SIGNATURES = {
     "lo_csr_destroy": (cint, [P]),
     "lo_csr_struct_info": (cint, [P, P, P]),
     "lo_reorder_pcb": (cint, [P, C.c_char_p, cint, cint, PP]),
+    "lo_locality_histogram": (cint, [P, P, P, P, P, P, P, P, u64]),
     "lo_coded_write_pcb": (cint, [P, P, C.c_char_p]),
     "lo_octree_from_leaves": (cint, [P, P, P, P, u64, P, cint, cint, u32, PP]),
     "lo_octree_save": (cint, [P, P, C.c_char_p]),

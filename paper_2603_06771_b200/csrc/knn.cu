@@ -242,6 +242,47 @@ __global__ void locality_kernel(const u32* __restrict__ idx, u64 m, u32 keff,
     if (threadIdx.x < 33 && sb[threadIdx.x]) atomicAdd(&bins[threadIdx.x], sb[threadIdx.x]);
 }
 
+// Exact locality histogram (locality.cpp:41-97): count of every |map(i) - map(j)| into a dense
+// u64 array over d in [0, n); small d (the bulk for SFC orders) goes through a per-block
+// shared-memory histogram first, so the hot bins see no global atomic contention.
+constexpr u32 kLocSmall = 4096;
+__global__ void locality_dense(const u32* __restrict__ idx, u64 m, u32 keff,
+                               const u32* __restrict__ centres, const u32* __restrict__ map,
+                               unsigned long long* __restrict__ dense) {
+    __shared__ u32 sh[kLocSmall];
+    for (u32 i = threadIdx.x; i < kLocSmall; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < m * keff;
+         e += (u64)gridDim.x * blockDim.x) {
+        const u64 r = e / keff;
+        const u32 ci = centres ? centres[r] : static_cast<u32>(r);
+        const u32 mi = map ? map[ci] : ci;
+        const u32 mj = map ? map[idx[e]] : idx[e];
+        const u32 d = mi > mj ? mi - mj : mj - mi;
+        if (d < kLocSmall) atomicAdd(&sh[d], 1u);
+        else atomicAdd(&dense[d], 1ull);
+    }
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < kLocSmall; i += blockDim.x)
+        if (sh[i]) atomicAdd(&dense[i], static_cast<unsigned long long>(sh[i]));
+}
+
+__global__ void nonzero_flags(const unsigned long long* __restrict__ dense, u64 n, u32* __restrict__ f) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        f[i] = dense[i] != 0;
+}
+
+__global__ void compact_bins(const unsigned long long* __restrict__ dense, const u64* __restrict__ pos,
+                             u64 n, u32* __restrict__ d_out, u64* __restrict__ c_out) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const unsigned long long c = dense[i];
+        if (c) {
+            d_out[pos[i]] = static_cast<u32>(i);
+            c_out[pos[i]] = c;
+        }
+    }
+}
+
 // seed_base >= 0: query i is cloud point seed_base + i (Full / range mode), which lets each
 // tile seed its heaps from the contiguous SFC window around it.
 static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_coded* c, u32 k,
@@ -459,6 +500,61 @@ int lo_locality_log2(lo_context* ctx, const lo_knn_result* res, const lo_coded* 
         dfree(ctx, bins);
         dfree(ctx, cidx);
         sync(ctx);
+    });
+}
+
+int lo_locality_histogram(lo_context* ctx, const lo_knn_result* res, const lo_coded* coded,
+                          const uint32_t* centres_host, const uint32_t* index_map_host,
+                          uint64_t* nbins, uint32_t* d_host, uint64_t* count_host, uint64_t cap) {
+    return api([&] {
+        require(res && coded && nbins, LO_INVALID_ARGUMENT, "null argument");
+        const u64 n = coded->n;
+        u32* cidx = upload_centres(ctx, centres_host, centres_host ? res->rows : 0, n);
+        u32* map = nullptr;
+        unsigned long long* dense = nullptr;
+        u32* flags = nullptr;
+        u64* pos = nullptr;
+        u32* dd = nullptr;
+        u64* cc = nullptr;
+        auto release = [&] {
+            dfree(ctx, cidx), dfree(ctx, map), dfree(ctx, dense), dfree(ctx, flags), dfree(ctx, pos);
+            dfree(ctx, dd), dfree(ctx, cc);
+        };
+        try {
+            if (index_map_host) {
+                map = dalloc_t<u32>(ctx, n);
+                LO_CUDA(cudaMemcpyAsync(map, index_map_host, 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+            }
+            dense = dalloc_t<unsigned long long>(ctx, n);
+            LO_CUDA(cudaMemsetAsync(dense, 0, 8 * n, ctx->stream));
+            const u64 e = res->rows * res->keff;
+            if (e) {
+                locality_dense<<<std::max(1, std::min(ceil_div(e, 256), ctx->sm_count * 4)), 256, 0,
+                                 ctx->stream>>>(res->idx, res->rows, res->keff, cidx, map, dense);
+                LO_CHECK_LAUNCH();
+            }
+            flags = dalloc_t<u32>(ctx, n);
+            pos = dalloc_t<u64>(ctx, n + 1);
+            const int g = std::max(1, std::min(ceil_div(n, 256), ctx->sm_count * 16));
+            nonzero_flags<<<g, 256, 0, ctx->stream>>>(dense, n, flags);
+            LO_CHECK_LAUNCH();
+            exclusive_scan_u32_to_u64(ctx, flags, pos, n);
+            const u64 nb = read_scalar(ctx, pos + n);
+            *nbins = nb;
+            if (d_host && count_host && nb <= cap && nb) {
+                dd = dalloc_t<u32>(ctx, nb);
+                cc = dalloc_t<u64>(ctx, nb);
+                compact_bins<<<g, 256, 0, ctx->stream>>>(dense, pos, n, dd, cc);
+                LO_CHECK_LAUNCH();
+                LO_CUDA(cudaMemcpyAsync(d_host, dd, 4 * nb, cudaMemcpyDeviceToHost, ctx->stream));
+                LO_CUDA(cudaMemcpyAsync(count_host, cc, 8 * nb, cudaMemcpyDeviceToHost, ctx->stream));
+            }
+            sync(ctx);
+        } catch (...) {
+            release();
+            throw;
+        }
+        release();
     });
 }
 

@@ -783,3 +783,154 @@ def generate_mixed(n: int, seed: int) -> np.ndarray:
     a = np.empty((n, 3))
     check(_lib.lib().lo_generate_mixed(n, seed, _p(a)))
     return a
+
+
+# ---- locality (locality.hpp / locality.cpp) ------------------------------------------------
+@dataclass
+class LocalityHistogram:
+    """locality.hpp:18-40: bins = ascending distinct |i - j| with their counts."""
+    k: int
+    cloud_size: int
+    centres: int
+    d: np.ndarray      # u32, ascending
+    count: np.ndarray  # u64
+
+    @property
+    def bins(self):
+        return list(zip(self.d.tolist(), self.count.tolist()))
+
+    def total(self) -> int:
+        return int(self.count.sum(dtype=np.uint64))
+
+    def count_at(self, d: int) -> int:
+        i = int(np.searchsorted(self.d, d))
+        return int(self.count[i]) if i < len(self.d) and self.d[i] == d else 0
+
+    # sequential left-to-right double accumulation, as locality.cpp:19-37 (np.cumsum is
+    # sequential; np.sum would be pairwise and round differently)
+    def mean(self) -> float:
+        t = self.total()
+        if t == 0:
+            return 0.0
+        s = np.cumsum(self.d.astype(np.float64) * self.count.astype(np.float64))[-1]
+        return float(s / float(t))
+
+    def stddev(self) -> float:
+        t = self.total()
+        if t == 0:
+            return 0.0
+        dd = self.d.astype(np.float64) - self.mean()
+        s = np.cumsum(dd * dd * self.count.astype(np.float64))[-1]
+        return float(np.sqrt(s / float(t)))
+
+
+def fisher_pearson_skewness(h: LocalityHistogram) -> float:
+    """locality.cpp:112-125."""
+    t = h.total()
+    if t == 0:
+        return 0.0
+    mu, sigma = h.mean(), h.stddev()
+    if sigma == 0.0:
+        return 0.0
+    z = (h.d.astype(np.float64) - mu) / sigma
+    s = np.cumsum(z * z * z * h.count.astype(np.float64))[-1]
+    return float(s / float(t))
+
+
+def histogram_quantiles(h: LocalityHistogram):
+    """locality.cpp:127-140: smallest d whose cumulative count reaches 25 / 50 / 75 % of the mass."""
+    t = h.total()
+    out = [0.0, 0.0, 0.0]
+    if t == 0:
+        return out
+    cum = np.cumsum(h.count.astype(np.uint64))
+    for qi, q in enumerate((0.25, 0.5, 0.75)):
+        i = int(np.argmax(cum.astype(np.float64) >= q * float(t)))
+        out[qi] = float(h.d[i])
+    return out
+
+
+def _locality(tree: LinearOctree, coded: CodedCloud, k: int, centres, index_map) -> LocalityHistogram:
+    n = coded.n
+    if k < 1:
+        raise InvalidArgument("locality histogram: k must be >= 1")
+    if k > n:
+        raise InvalidArgument("locality histogram: k exceeds cloud size")
+    imap = None
+    if index_map is not None:
+        imap = np.ascontiguousarray(index_map, np.uint32)
+        if len(imap) != n:
+            raise InvalidArgument("locality histogram: index map size mismatch")
+    L = _lib.lib()
+    ctx = coded.ctx
+    res = C.c_void_p()
+    m = n if centres is None else len(centres)
+    check(L.lo_knn(ctx.h, tree.h, coded.h, int(k), _p(centres), 0 if centres is None else m, 0, C.byref(res)))
+    try:
+        nb = C.c_uint64()
+        check(L.lo_locality_histogram(ctx.h, res, coded.h, _p(centres), _p(imap), C.byref(nb), None, None, 0))
+        d = np.empty(nb.value, np.uint32)
+        c = np.empty(nb.value, np.uint64)
+        check(L.lo_locality_histogram(ctx.h, res, coded.h, _p(centres), _p(imap), C.byref(nb), _p(d), _p(c),
+                                      len(d)))
+    finally:
+        L.lo_knn_destroy(res)
+    return LocalityHistogram(int(k), n, m, d, c)
+
+
+def locality_histogram(tree: LinearOctree, coded: CodedCloud, k: int, threads: int = 1,
+                       index_map=None) -> LocalityHistogram:
+    """locality.hpp:49-51: exact histogram over every centre (index_map: e.g. coded.permutation
+    to measure the original storage order)."""
+    return _locality(tree, coded, k, None, index_map)
+
+
+def locality_histogram_approx(tree: LinearOctree, coded: CodedCloud, k: int, sample_size: int, seed: int,
+                              threads: int = 1, index_map=None) -> LocalityHistogram:
+    """locality.hpp:55-58: over sample_indices(n, sample_size, seed)."""
+    if sample_size > coded.n:
+        raise InvalidArgument("locality histogram: sample size exceeds cloud size")
+    return _locality(tree, coded, k, sample_indices(coded.n, sample_size, seed), index_map)
+
+
+# ---- memory model (memory_model.hpp / memory_model.cpp) ------------------------------------
+@dataclass
+class MemoryReport:
+    """memory_model.hpp:27-45 for the linear octree; `device_bytes` adds what the B200 path keeps
+    resident beyond the reference's arrays (traversal table, FP32 shadow)."""
+    bytes_total: int
+    node_count: int
+    point_count: int
+    device_bytes: int = 0
+
+    def rho(self) -> float:
+        return 0.0 if self.point_count == 0 else self.node_count / self.point_count
+
+    def overhead(self, point_bytes: float = 32.0) -> float:
+        return self.bytes_total / (point_bytes * self.point_count)
+
+
+def measure_structure(tree: LinearOctree) -> MemoryReport:
+    """memory_model.cpp:21-30: boundaries (8 B) + offsets (4 B) per leaf + 1, 56 B per internal node."""
+    L = tree.leaf_count()
+    b = (L + 1) * 8 + (L + 1) * 4 + tree.internal_count() * 56
+    dev = b + int(tree.info.tnodes) * (64 + 48)
+    return MemoryReport(b, tree.node_count(), tree.point_count(), dev)
+
+
+@dataclass
+class StructureCostParams:
+    """memory_model.hpp:13-24."""
+    node_bytes: float = 0.0
+    point_extra_bytes: float = 0.0
+    nodes_per_point: float = 0.0
+    point_bytes: float = 32.0
+
+
+def expected_overhead(p: StructureCostParams) -> float:
+    return (p.point_extra_bytes + p.nodes_per_point * p.node_bytes) / p.point_bytes
+
+
+def linear_octree_cost_params(rho: float) -> StructureCostParams:
+    """memory_model.cpp:39-43: 7 leaves (12 B) per 56 B internal node."""
+    return StructureCostParams((7.0 * 12.0 + 56.0) / 8.0, 0.0, rho, 32.0)
