@@ -11,7 +11,9 @@
 //                                             KernelShape::Sphere, 2.5, BatchOptions{});
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -450,6 +452,132 @@ inline RangedResult neighbours_struct(const LinearOctree& tree, const CodedCloud
                                   static_cast<int>(shape), radius, &center.x, 1, &h));
     std::unique_ptr<lo_csr, int (*)(lo_csr*)> guard(h, &lo_csr_destroy);
     return std::move(struct_rows(coded.context(), h, 1)[0]);
+}
+
+// ---- locality (locality.hpp / locality.cpp) -------------------------------------------------
+struct LocalityHistogram {  // locality.hpp:18-40
+    std::uint32_t k = 0;
+    std::uint64_t cloud_size = 0;
+    std::uint64_t centres = 0;
+    std::vector<std::pair<std::uint32_t, std::uint64_t>> bins;  // (d, count), ascending d
+    std::uint64_t total() const {
+        std::uint64_t t = 0;
+        for (const auto& [d, c] : bins) t += c;
+        return t;
+    }
+    std::uint64_t count_at(std::uint32_t d) const {
+        auto it = std::lower_bound(bins.begin(), bins.end(), d,
+                                   [](const auto& b, std::uint32_t v) { return b.first < v; });
+        return it != bins.end() && it->first == d ? it->second : 0;
+    }
+    double mean() const {
+        const std::uint64_t t = total();
+        if (t == 0) return 0.0;
+        double s = 0.0;
+        for (const auto& [d, c] : bins) s += static_cast<double>(d) * static_cast<double>(c);
+        return s / static_cast<double>(t);
+    }
+    double stddev() const {
+        const std::uint64_t t = total();
+        if (t == 0) return 0.0;
+        const double mu = mean();
+        double s = 0.0;
+        for (const auto& [d, c] : bins) {
+            const double dd = static_cast<double>(d) - mu;
+            s += dd * dd * static_cast<double>(c);
+        }
+        return std::sqrt(s / static_cast<double>(t));
+    }
+};
+
+namespace detail {
+inline LocalityHistogram locality(const LinearOctree& tree, const CodedCloud& coded, std::uint32_t k,
+                                  const std::vector<std::uint32_t>& centres,
+                                  const std::vector<std::uint32_t>* index_map) {
+    const std::uint64_t n = coded.size();
+    if (k < 1) throw std::invalid_argument("locality histogram: k must be >= 1");
+    if (k > n) throw std::invalid_argument("locality histogram: k exceeds cloud size");
+    if (index_map && index_map->size() != n)
+        throw std::invalid_argument("locality histogram: index map size mismatch");
+    lo_context* ctx = coded.context().get();
+    lo_knn_result* h = nullptr;
+    check(lo_knn(ctx, tree.handle(), coded.handle(), k, centres.empty() ? nullptr : centres.data(),
+                 centres.size(), 0, &h));
+    std::unique_ptr<lo_knn_result, int (*)(lo_knn_result*)> guard(h, &lo_knn_destroy);
+    const std::uint32_t* c = centres.empty() ? nullptr : centres.data();
+    const std::uint32_t* m = index_map ? index_map->data() : nullptr;
+    std::uint64_t nb = 0;
+    check(lo_locality_histogram(ctx, h, coded.handle(), c, m, &nb, nullptr, nullptr, 0));
+    std::vector<std::uint32_t> d(nb);
+    std::vector<std::uint64_t> cnt(nb);
+    check(lo_locality_histogram(ctx, h, coded.handle(), c, m, &nb, d.data(), cnt.data(), nb));
+    LocalityHistogram out;
+    out.k = k;
+    out.cloud_size = n;
+    out.centres = centres.empty() ? n : centres.size();
+    out.bins.resize(nb);
+    for (std::uint64_t i = 0; i < nb; ++i) out.bins[i] = {d[i], cnt[i]};
+    return out;
+}
+}  // namespace detail
+
+// locality.hpp:49-58 (threads accepted, ignored)
+inline LocalityHistogram locality_histogram(const LinearOctree& tree, const CodedCloud& coded,
+                                            std::uint32_t k, int /*threads*/ = 1,
+                                            const std::vector<std::uint32_t>* index_map = nullptr) {
+    return detail::locality(tree, coded, k, {}, index_map);
+}
+inline LocalityHistogram locality_histogram_approx(const LinearOctree& tree, const CodedCloud& coded,
+                                                   std::uint32_t k, std::uint32_t sample_size,
+                                                   std::uint64_t seed, int /*threads*/ = 1,
+                                                   const std::vector<std::uint32_t>* index_map = nullptr) {
+    if (sample_size > coded.size())
+        throw std::invalid_argument("locality histogram: sample size exceeds cloud size");
+    std::vector<std::uint32_t> c(sample_size);
+    check(lo_sample_indices(static_cast<std::uint32_t>(coded.size()), sample_size, seed, c.data()));
+    return detail::locality(tree, coded, k, c, index_map);
+}
+// locality.cpp:112-140
+inline double fisher_pearson_skewness(const LocalityHistogram& h) {
+    const std::uint64_t t = h.total();
+    if (t == 0) return 0.0;
+    const double mu = h.mean(), sigma = h.stddev();
+    if (sigma == 0.0) return 0.0;
+    double s = 0.0;
+    for (const auto& [d, c] : h.bins) {
+        const double z = (static_cast<double>(d) - mu) / sigma;
+        s += z * z * z * static_cast<double>(c);
+    }
+    return s / static_cast<double>(t);
+}
+inline std::array<double, 3> histogram_quantiles(const LocalityHistogram& h) {
+    const std::uint64_t t = h.total();
+    std::array<double, 3> out{0.0, 0.0, 0.0};
+    if (t == 0) return out;
+    const std::array<double, 3> q{0.25, 0.5, 0.75};
+    std::uint64_t cum = 0;
+    std::size_t qi = 0;
+    for (const auto& [d, c] : h.bins) {
+        cum += c;
+        while (qi < 3 && static_cast<double>(cum) >= q[qi] * static_cast<double>(t)) out[qi++] = d;
+        if (qi == 3) break;
+    }
+    return out;
+}
+
+// ---- memory model (memory_model.hpp:13-58) --------------------------------------------------
+struct MemoryReport {
+    std::uint64_t bytes_total = 0, node_count = 0, point_count = 0;
+    double rho() const { return point_count == 0 ? 0.0 : double(node_count) / double(point_count); }
+    double overhead(double point_bytes = 32.0) const { return double(bytes_total) / (point_bytes * double(point_count)); }
+};
+inline MemoryReport measure_structure(const LinearOctree& tree) {
+    MemoryReport r;
+    r.node_count = tree.node_count();
+    r.point_count = tree.point_count();
+    r.bytes_total = (tree.leaf_count() + 1) * (sizeof(std::uint64_t) + sizeof(std::uint32_t)) +
+                    tree.internal_count() * sizeof(lo_internal_node);
+    return r;
 }
 
 }  // namespace linoct::b200

@@ -117,6 +117,12 @@ int main() {
         EXPECT(throws<std::runtime_error>([&] { reorder_pcb("/nonexistent/x.pcb", curve); }));
         std::remove(loc.c_str());
         std::remove(pcb.c_str());
+        auto hist = locality_histogram(tree, coded, 8);
+        EXPECT(hist.total() == 8ull * n && hist.count_at(0) == n);
+        auto qs = histogram_quantiles(hist);
+        EXPECT(qs[0] <= qs[1] && qs[1] <= qs[2] && hist.stddev() > 0.0 && fisher_pearson_skewness(hist) > 0.0);
+        auto mem = measure_structure(tree);
+        EXPECT(mem.node_count == tree.node_count() && mem.bytes_total > 0);
         auto all = neighbours_struct(tree, coded, KernelShape::Sphere, {50, 50, 50}, 1e5);
         EXPECT(all.ranges.size() == 1 && all.ranges[0].first == 0 && all.ranges[0].second == n &&
                all.singles.empty());
