@@ -359,10 +359,13 @@ def run_ours(args, cfg):
             _lib.check(L.lo_host_alloc_pinned(24 * n, C.byref(pinned)))
             C.memmove(pinned, xyz_host.ctypes.data, 24 * n)
         rows = b1 - b0
-        hc = C.c_void_p()
-        hf = C.c_void_p()
-        _lib.check(L.lo_host_alloc_pinned(4 * max(rows, 1), C.byref(hc)))
-        _lib.check(L.lo_host_alloc_pinned(8 * max(rows, 1), C.byref(hf)))
+        # one pinned (counts, digests) pair per radius: radius i's results travel on the copy
+        # stream while radius i + 1 computes (lo_csr_download_async)
+        hc = [C.c_void_p() for _ in radii]
+        hf = [C.c_void_p() for _ in radii]
+        for a, b in zip(hc, hf):
+            _lib.check(L.lo_host_alloc_pinned(4 * max(rows, 1), C.byref(a)))
+            _lib.check(L.lo_host_alloc_pinned(8 * max(rows, 1), C.byref(b)))
 
         def e2e_step():
             coded = tree = None
@@ -373,12 +376,13 @@ def run_ours(args, cfg):
                 _lib.check(L.lo_octree_build(ctx.h, coded, cfg["n_max"], C.byref(tree)))
             if world > 1:
                 coded, tree, _, _ = D.broadcast_structure(ctx, coded, tree, src=0)
-            for r in radii:
+            for i, r in enumerate(radii):
                 csr = C.c_void_p()
                 _lib.check(L.lo_radius_range(ctx.h, tree, coded, 1, 0, r, b0, b1, 1, C.byref(csr)))
-                _lib.check(L.lo_csr_download(ctx.h, csr, hc, hf, None, None))
+                _lib.check(L.lo_csr_download_async(ctx.h, csr, hc[i], hf[i], None, None))
                 L.lo_csr_destroy(csr)
             free(coded, tree)
+            _lib.check(L.lo_context_synchronize(ctx.h))
 
         for _ in range(max(1, args.warmup // 2)):
             e2e_step()
@@ -400,11 +404,13 @@ def run_ours(args, cfg):
         e2e = {"value": len(radii) * n / (ems * 1e-3), "unit": "queries/s", "ms_per_step": ems,
                "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": len(radii) * 12 * n,
                "path": "lo_reorder(host pinned) -> lo_octree_build -> lo_radius_range(+FNV) -> "
-                       "lo_csr_download(counts, digests)"}
+                       "lo_csr_download_async(counts, digests; overlapped with the next radius) -> "
+                       "lo_context_synchronize"}
         if rank == 0:
             L.lo_host_free_pinned(pinned)
-        L.lo_host_free_pinned(hc)
-        L.lo_host_free_pinned(hf)
+        for a, b in zip(hc, hf):
+            L.lo_host_free_pinned(a)
+            L.lo_host_free_pinned(b)
 
     # roofline of the dominant kernel (largest device time in the step)
     mus = {r: totals[r] / max(1, b1 - b0) for r in radii}

@@ -96,6 +96,7 @@ int lo_device_count(int* count);
  * otherwise work is enqueued on the given cudaStream_t (e.g. torch's current stream). */
 int lo_context_create(int device, void* stream, lo_context** out);
 int lo_context_destroy(lo_context* ctx);
+/* Waits for the context's compute and copy streams (async downloads included). */
 int lo_context_synchronize(lo_context* ctx);
 void* lo_context_stream(lo_context* ctx);
 /* Per-stage device timers (CUDA events on the context stream); off by default. */
@@ -211,6 +212,13 @@ int lo_csr_info_get(const lo_csr* csr, lo_csr_info* out);
 /* counts[m], fingerprints[m] (FNV-1a-64, search.cpp:263-271), offsets[m+1], indices[total]. */
 int lo_csr_download(lo_context* ctx, const lo_csr* csr, uint32_t* counts_host,
                     uint64_t* fingerprints_host, uint64_t* offsets_host, uint32_t* indices_host);
+/* Same, asynchronously: the copies run on the context's copy stream after the result is
+ * complete, so the next batch computes while this one's results travel (use pinned host
+ * buffers, lo_host_alloc_pinned).  The host buffers are filled once lo_context_synchronize
+ * returns; the result may be destroyed before that (its device buffers are released when the
+ * copy has finished). */
+int lo_csr_download_async(lo_context* ctx, lo_csr* csr, uint32_t* counts_host,
+                          uint64_t* fingerprints_host, uint64_t* offsets_host, uint32_t* indices_host);
 int lo_csr_device_ptrs(const lo_csr* csr, const uint64_t** offsets, const uint32_t** indices);
 /* RadiusMethod::Struct results (neighbours_struct, search.cpp:76-135; RangedResult,
  * search.hpp:18-56): per row the coalesced contained ranges and the singles, each as a CSR

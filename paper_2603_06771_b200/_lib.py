@@ -77,6 +77,7 @@ SIGNATURES = {
     "lo_csr_info_get": (cint, [P, C.POINTER(CsrInfo)]),
     "lo_csr_download": (cint, [P, P, P, P, P, P]),
     "lo_csr_device_ptrs": (cint, [P, PP, PP]),
+    "lo_csr_download_async": (cint, [P, P, P, P, P, P]),
     "lo_csr_destroy": (cint, [P]),
     "lo_csr_struct_info": (cint, [P, P, P]),
     "lo_reorder_pcb": (cint, [P, C.c_char_p, cint, cint, PP]),

@@ -28,7 +28,24 @@ void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
     throw Error(LO_CUDA_ERROR, buf);
 }
 
+void reclaim(lo_context* ctx, bool wait) {
+    auto& d = ctx->deferred;
+    for (size_t i = 0; i < d.size();) {
+        if (wait) cudaEventSynchronize(d[i].done);
+        if (cudaEventQuery(d[i].done) == cudaSuccess) {
+            for (void* p : d[i].ptrs) cudaFreeAsync(p, ctx->stream);
+            cudaEventDestroy(d[i].done);
+            d[i] = d.back();
+            d.pop_back();
+        } else {
+            cudaGetLastError();  // cudaErrorNotReady is not an error
+            ++i;
+        }
+    }
+}
+
 void* dalloc(lo_context* ctx, size_t bytes) {
+    if (!ctx->deferred.empty()) reclaim(ctx, false);
     void* p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, bytes, ctx->stream);
     if (e != cudaSuccess) {
@@ -359,6 +376,7 @@ int lo_context_create(int device, void* stream, lo_context** out) {
             LO_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
             ctx->own_stream = true;
         }
+        LO_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         cudaMemPool_t pool;
         LO_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
         u64 threshold = ~0ull;
@@ -373,6 +391,10 @@ int lo_context_destroy(lo_context* ctx) {
     return api([&] {
         if (!ctx) return;
         cudaStreamSynchronize(ctx->stream);
+        if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+        reclaim(ctx, true);
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
         for (auto& s : ctx->stages) {
             cudaEventDestroy(s.a);
             cudaEventDestroy(s.b);
@@ -384,7 +406,13 @@ int lo_context_destroy(lo_context* ctx) {
     });
 }
 
-int lo_context_synchronize(lo_context* ctx) { return api([&] { sync(ctx); }); }
+int lo_context_synchronize(lo_context* ctx) {
+    return api([&] {
+        sync(ctx);
+        LO_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+        reclaim(ctx, true);
+    });
+}
 void* lo_context_stream(lo_context* ctx) { return ctx ? ctx->stream : nullptr; }
 
 int lo_context_set_timing(lo_context* ctx, int enabled) {

@@ -100,6 +100,15 @@ struct lo_context {
     void* pinned_scratch = nullptr;     // small pinned buffer for scalar D2H
     void* arena = nullptr;              // persistent device scratch (radius records)
     size_t arena_bytes = 0;
+    // asynchronous result downloads (lo_csr_download_async): D2H on a second stream so the
+    // next batch computes while the previous one's results travel; buffers of results destroyed
+    // while their copy is in flight are released once the copy has completed.
+    cudaStream_t copy_stream = nullptr;
+    struct Deferred {
+        cudaEvent_t done;
+        std::vector<void*> ptrs;
+    };
+    std::vector<Deferred> deferred;
 };
 
 struct lo_coded {
@@ -161,6 +170,8 @@ struct lo_csr {
     lo::u32* ranges = nullptr;          // [2*total_ranges]
     lo::u64* single_offsets = nullptr;  // [rows+1]
     lo::u32* singles = nullptr;         // [total_singles]
+    cudaEvent_t copied = nullptr;       // last lo_csr_download_async (null: none pending)
+    unsigned copy_mask = 0;             // buffers it reads: 1 counts, 2 fps, 4 offsets, 8 indices
 };
 
 namespace lo {
@@ -192,6 +203,8 @@ namespace lo {
 
 // ---- memory + timing helpers (context.cu) ------------------------------------------------
 void* dalloc(lo_context* ctx, size_t bytes);
+// Releases deferred buffers whose async copies finished (all of them when wait is true).
+void reclaim(lo_context* ctx, bool wait);
 void dfree(lo_context* ctx, void* p);
 template <class T>
 T* dalloc_t(lo_context* ctx, size_t count) {

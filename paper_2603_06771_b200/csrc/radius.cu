@@ -86,14 +86,25 @@ __global__ void __launch_bounds__(kRadiusThreads) radius_kernel(
     }
 }
 
-// K8: FNV-1a-64 per row over its indices (search.cpp:345-347).
+// K8: FNV-1a-64 per row over its indices (search.cpp:345-347).  The hash chain is sequential
+// per row, so a thread owns a row; it reads the row with 16-byte loads (one L1 sector per load
+// instead of one per index) after peeling to 16-byte alignment.
 __global__ void radius_digest(const u64* __restrict__ offsets, const u32* __restrict__ idx, u64 m,
                               u64* __restrict__ fps) {
     for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < m;
          r += (u64)gridDim.x * blockDim.x) {
         u64 h = kFnvOffset;
+        u64 j = offsets[r];
         const u64 e = offsets[r + 1];
-        for (u64 j = offsets[r]; j < e; ++j) h = fnv_u32(h, idx[j]);
+        for (; j < e && (j & 3); ++j) h = fnv_u32(h, __ldg(idx + j));
+        for (; j + 4 <= e; j += 4) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(idx + j));
+            h = fnv_u32(h, v.x);
+            h = fnv_u32(h, v.y);
+            h = fnv_u32(h, v.z);
+            h = fnv_u32(h, v.w);
+        }
+        for (; j < e; ++j) h = fnv_u32(h, __ldg(idx + j));
         fps[r] = h;
     }
 }
@@ -451,6 +462,33 @@ int lo_csr_download(lo_context* ctx, const lo_csr* csr, uint32_t* counts_host,
                                     cudaMemcpyDeviceToHost, ctx->stream));
         }
         sync(ctx);
+    });
+}
+
+int lo_csr_download_async(lo_context* ctx, lo_csr* csr, uint32_t* counts_host,
+                          uint64_t* fingerprints_host, uint64_t* offsets_host, uint32_t* indices_host) {
+    return api([&] {
+        require(csr != nullptr, LO_INVALID_ARGUMENT, "null result");
+        require(!fingerprints_host || csr->fps, LO_INVALID_ARGUMENT, "fingerprints were not computed");
+        if (indices_host && csr->total) ensure_expanded(ctx, csr);
+        if (!csr->copied) LO_CUDA(cudaEventCreateWithFlags(&csr->copied, cudaEventDisableTiming));
+        cudaEvent_t ready;
+        LO_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        LO_CUDA(cudaEventRecord(ready, ctx->stream));
+        LO_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
+        cudaEventDestroy(ready);  // released once the recorded work completes
+        cudaStream_t s = ctx->copy_stream;
+        csr->copy_mask |= (counts_host ? 1u : 0u) | (fingerprints_host ? 2u : 0u) | (offsets_host ? 4u : 0u) |
+                          (indices_host ? 8u : 0u);
+        if (counts_host && csr->rows)
+            LO_CUDA(cudaMemcpyAsync(counts_host, csr->counts, 4 * csr->rows, cudaMemcpyDeviceToHost, s));
+        if (fingerprints_host && csr->rows)
+            LO_CUDA(cudaMemcpyAsync(fingerprints_host, csr->fps, 8 * csr->rows, cudaMemcpyDeviceToHost, s));
+        if (offsets_host)
+            LO_CUDA(cudaMemcpyAsync(offsets_host, csr->offsets, 8 * (csr->rows + 1), cudaMemcpyDeviceToHost, s));
+        if (indices_host && csr->total)
+            LO_CUDA(cudaMemcpyAsync(indices_host, csr->indices, 4 * csr->total, cudaMemcpyDeviceToHost, s));
+        LO_CUDA(cudaEventRecord(csr->copied, s));
     });
 }
 

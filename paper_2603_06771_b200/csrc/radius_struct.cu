@@ -250,6 +250,25 @@ void ensure_expanded(lo_context* ctx, lo_csr* csr) {
 }
 
 void free_csr_buffers(lo_context* ctx, lo_csr* csr) {
+    if (csr->copied) {
+        if (cudaEventQuery(csr->copied) != cudaSuccess) {
+            // an async download still reads some buffers: release those once it has finished
+            cudaGetLastError();
+            lo_context::Deferred d{csr->copied, {}};
+            void** bufs[4] = {reinterpret_cast<void**>(&csr->counts), reinterpret_cast<void**>(&csr->fps),
+                              reinterpret_cast<void**>(&csr->offsets), reinterpret_cast<void**>(&csr->indices)};
+            for (int b = 0; b < 4; ++b)
+                if ((csr->copy_mask >> b) & 1u && *bufs[b]) {
+                    d.ptrs.push_back(*bufs[b]);
+                    *bufs[b] = nullptr;
+                }
+            ctx->deferred.push_back(std::move(d));
+        } else {
+            cudaEventDestroy(csr->copied);
+        }
+        csr->copied = nullptr;
+        csr->copy_mask = 0;
+    }
     dfree(ctx, csr->counts);
     dfree(ctx, csr->offsets);
     dfree(ctx, csr->indices);
