@@ -24,11 +24,11 @@ struct PtShared {
     u32 stack[kStackCap];
     float4 buf[32];      // candidate (x, y, z) relative FP32, .w = point index bits
     float4 qf[32];       // queries, FP32
-    __align__(8) float qx[32];  // queries, FP32 SoA: (q[2p], q[2p+1]) loads as one f32x2
-    __align__(8) float qy[32];
-    __align__(8) float qz[32];
+    __align__(16) float qx[32];  // queries, FP32 SoA: (q[2p], q[2p+1]) loads as one f32x2
+    __align__(16) float qy[32];
+    __align__(16) float qz[32];
     double qd[32][3];    // queries, FP64 (band decisions)
-    __align__(8) u32 msk[32];  // count pass: membership ballot of query L for the current buffer
+    __align__(16) u32 msk[32];  // count pass: membership ballot of query L for the current buffer
 };
 
 // Decide band lanes exactly; returns the corrected membership ballot for query L.
@@ -65,6 +65,49 @@ __device__ __forceinline__ void process_buffer(PtShared& S, u32 fill, u32 qmask,
     const u32 lt = (1u << lane) - 1u;
     const u32 lo_bits = __float_as_uint(lo_thr);
     const u32 band_bits = __float_as_uint(hi_thr) - lo_bits;
+    if (!FILL && kPacked) {
+        // count pass: four queries (two packed pairs) per iteration -- one band vote, one
+        // 16-byte mask store and one loop step for four membership ballots
+        u32 qm = (qmask | (qmask >> 1) | (qmask >> 2) | (qmask >> 3)) & 0x11111111u;
+        S.msk[lane] = 0u;
+        __syncwarp();
+        while (qm) {
+            const int b = __ffs(qm) - 1;  // = 4q
+            qm &= qm - 1;
+            const float4 X = *reinterpret_cast<const float4*>(&S.qx[b]);
+            const float4 Y = *reinterpret_cast<const float4*>(&S.qy[b]);
+            const u64 dxa = fsub2(PX, pack2(X.x, X.y)), dxb = fsub2(PX, pack2(X.z, X.w));
+            const u64 dya = fsub2(PY, pack2(Y.x, Y.y)), dyb = fsub2(PY, pack2(Y.z, Y.w));
+            u64 da = fmul2(dxa, dxa), db = fmul2(dxb, dxb);
+            da = ffma2(dya, dya, da);
+            db = ffma2(dyb, dyb, db);
+            if (SHAPE == LO_SPHERE) {
+                const float4 Z = *reinterpret_cast<const float4*>(&S.qz[b]);
+                const u64 dza = fsub2(PZ, pack2(Z.x, Z.y)), dzb = fsub2(PZ, pack2(Z.z, Z.w));
+                da = ffma2(dza, dza, da);
+                db = ffma2(dzb, dzb, db);
+            }
+            float v[4];
+            unpack2(da, v[0], v[1]);
+            unpack2(db, v[2], v[3]);
+            u32 in[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) in[t] = __ballot_sync(~0u, v[t] < lo_thr);
+            const u32 w01 = min(__float_as_uint(v[0]) - lo_bits, __float_as_uint(v[1]) - lo_bits);
+            const u32 w23 = min(__float_as_uint(v[2]) - lo_bits, __float_as_uint(v[3]) - lo_bits);
+            if (__any_sync(~0u, min(w01, w23) < band_bits)) {  // rare: band points, FP64 decides
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const u32 h = __ballot_sync(~0u, v[t] < hi_thr);
+                    if (h ^ in[t]) in[t] = band_fix<SHAPE>(in[t], h ^ in[t], S, b + t, lane, idx, px, py, pz, r, r2);
+                }
+            }
+            if (lane == 0) *reinterpret_cast<uint4*>(&S.msk[b]) = make_uint4(in[0], in[1], in[2], in[3]);
+        }
+        __syncwarp();
+        mymask = S.msk[lane];
+        return;
+    }
     u32 pm = (qmask | (qmask >> 1)) & 0x55555555u;  // bit 2p: pair p has an interested query
     if (!FILL) {
         S.msk[lane] = 0u;
