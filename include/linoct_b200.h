@@ -107,6 +107,12 @@ int lo_context_stage_times(lo_context* ctx, char* names, int name_len, double* m
 int lo_device_alloc(lo_context* ctx, uint64_t bytes, void** out_dev);
 int lo_device_free(lo_context* ctx, void* dev);
 int lo_memcpy_h2d(lo_context* ctx, void* dst_dev, const void* src_host, uint64_t bytes);
+/* Staged uploads for pipelined callers: lo_h2d_begin enqueues the copy on the context's upload
+ * stream and returns (use pinned host memory); lo_h2d_wait(slot) makes all work enqueued on the
+ * context afterwards wait for that copy -- e.g. upload batch i + 1 while batch i computes, then
+ * lo_h2d_wait + lo_reorder_device on it.  slot in [0, 4). */
+int lo_h2d_begin(lo_context* ctx, void* dst_dev, const void* src_host, uint64_t bytes, int slot);
+int lo_h2d_wait(lo_context* ctx, int slot);
 int lo_memcpy_d2h(lo_context* ctx, void* dst_host, const void* src_dev, uint64_t bytes);
 int lo_host_alloc_pinned(uint64_t bytes, void** out_host);
 int lo_host_free_pinned(void* host);

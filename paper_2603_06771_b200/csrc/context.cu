@@ -377,6 +377,8 @@ int lo_context_create(int device, void* stream, lo_context** out) {
             ctx->own_stream = true;
         }
         LO_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        LO_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+        for (auto& e : ctx->h2d_done) LO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         cudaMemPool_t pool;
         LO_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
         u64 threshold = ~0ull;
@@ -395,6 +397,12 @@ int lo_context_destroy(lo_context* ctx) {
         reclaim(ctx, true);
         cudaStreamSynchronize(ctx->stream);
         if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+        if (ctx->h2d_stream) {
+            cudaStreamSynchronize(ctx->h2d_stream);
+            cudaStreamDestroy(ctx->h2d_stream);
+        }
+        for (auto& e : ctx->h2d_done)
+            if (e) cudaEventDestroy(e);
         for (auto& s : ctx->stages) {
             cudaEventDestroy(s.a);
             cudaEventDestroy(s.b);
@@ -410,6 +418,7 @@ int lo_context_synchronize(lo_context* ctx) {
     return api([&] {
         sync(ctx);
         LO_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+        LO_CUDA(cudaStreamSynchronize(ctx->h2d_stream));
         reclaim(ctx, true);
     });
 }
@@ -456,6 +465,19 @@ int lo_memcpy_h2d(lo_context* ctx, void* dst, const void* src, uint64_t bytes) {
     return api([&] {
         LO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
         sync(ctx);
+    });
+}
+int lo_h2d_begin(lo_context* ctx, void* dst, const void* src, uint64_t bytes, int slot) {
+    return api([&] {
+        require(slot >= 0 && slot < lo_context::kH2dSlots, LO_INVALID_ARGUMENT, "h2d slot out of range");
+        LO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->h2d_stream));
+        LO_CUDA(cudaEventRecord(ctx->h2d_done[slot], ctx->h2d_stream));
+    });
+}
+int lo_h2d_wait(lo_context* ctx, int slot) {
+    return api([&] {
+        require(slot >= 0 && slot < lo_context::kH2dSlots, LO_INVALID_ARGUMENT, "h2d slot out of range");
+        LO_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->h2d_done[slot], 0));
     });
 }
 int lo_memcpy_d2h(lo_context* ctx, void* dst, const void* src, uint64_t bytes) {

@@ -109,6 +109,11 @@ struct lo_context {
         std::vector<void*> ptrs;
     };
     std::vector<Deferred> deferred;
+    // staged input uploads (lo_h2d_begin / lo_h2d_wait): their own stream so an upload for the
+    // next batch overlaps this batch's kernels and the D2H copies; one event per slot
+    cudaStream_t h2d_stream = nullptr;
+    static constexpr int kH2dSlots = 4;
+    cudaEvent_t h2d_done[kH2dSlots] = {};
 };
 
 struct lo_coded {
