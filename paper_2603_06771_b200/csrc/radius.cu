@@ -97,12 +97,25 @@ __global__ void radius_digest(const u64* __restrict__ offsets, const u32* __rest
         u64 j = offsets[r];
         const u64 e = offsets[r + 1];
         for (; j < e && (j & 3); ++j) h = fnv_u32(h, __ldg(idx + j));
-        for (; j + 4 <= e; j += 4) {
+        for (; j + 8 <= e; j += 8) {  // two loads in flight per iteration
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(idx + j));
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(idx + j + 4));
+            h = fnv_u32(h, v.x);
+            h = fnv_u32(h, v.y);
+            h = fnv_u32(h, v.z);
+            h = fnv_u32(h, v.w);
+            h = fnv_u32(h, u.x);
+            h = fnv_u32(h, u.y);
+            h = fnv_u32(h, u.z);
+            h = fnv_u32(h, u.w);
+        }
+        if (j + 4 <= e) {
             const uint4 v = __ldg(reinterpret_cast<const uint4*>(idx + j));
             h = fnv_u32(h, v.x);
             h = fnv_u32(h, v.y);
             h = fnv_u32(h, v.z);
             h = fnv_u32(h, v.w);
+            j += 4;
         }
         for (; j < e; ++j) h = fnv_u32(h, __ldg(idx + j));
         fps[r] = h;
