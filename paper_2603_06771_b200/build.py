@@ -15,7 +15,7 @@ OBJ = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "liblinoct_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CUDA_SOURCES = ["context.cu", "reorder.cu", "octree.cu", "radius.cu", "radius_struct.cu", "knn.cu", "io.cu"]
+CUDA_SOURCES = ["context.cu", "reorder.cu", "octree.cu", "radius.cu", "radius_struct.cu", "knn.cu", "io.cu", "centres.cu"]
 CXX_SOURCES = ["gen.cpp"]
 
 # -fmad=false: no DFMA contraction anywhere, the FP64 predicates must be the reference's

@@ -404,14 +404,17 @@ int lo_knn(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32
         const u64 rows = centres_host ? m : coded->n;
         ensure_float_shadows(ctx, coded, tree);
         u32* cidx = upload_centres(ctx, centres_host, m, coded->n);
-        Queries q{coded->x, coded->y, coded->z, cidx, rows, coded->pf, coded->bmax};
+        // explicit centres are searched in curve order, rows scattered back (centres.cu)
+        SortedCentres sc = sort_centres(ctx, cidx, centres_host ? m : 0);
+        Queries q{coded->x, coded->y, coded->z, centres_host ? sc.idx : nullptr, rows, coded->pf, coded->bmax};
         try {
-            *out = knn_search(ctx, tree, coded, k, q, fingerprint != 0, centres_host ? -1 : 0);
+            *out = knn_search(ctx, tree, coded, k, q, fingerprint != 0, centres_host ? kSeedSortedIdx : 0);
+            if (centres_host) unsort_knn(ctx, sc, *out);
         } catch (...) {
-            dfree(ctx, cidx);
+            dfree(ctx, cidx), dfree(ctx, sc.idx), dfree(ctx, sc.pos);
             throw;
         }
-        dfree(ctx, cidx);
+        dfree(ctx, cidx), dfree(ctx, sc.idx), dfree(ctx, sc.pos);
     });
 }
 

@@ -129,6 +129,7 @@ __device__ __forceinline__ void knn_stage(const KnnSmem& S, const float4* __rest
 }
 
 constexpr int kKnnFloatStack = kStackCap;
+constexpr i64 kSeedSortedIdx = -2;  // seed_base: queries are ascending cloud indices (q.idx)
 
 template <bool GLOBAL_HEAP>
 __global__ void __launch_bounds__(128) knn_float_kernel(
@@ -186,9 +187,17 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
 
         // 1) seed from the contiguous SFC window around the tile (Full / range mode)
         u32 skip_lo = 0, skip_hi = 0;
+        i64 t0 = 0, t1 = -1;
         if (seed_base >= 0) {
-            const i64 t0 = seed_base + static_cast<i64>(tile * 32);
-            const i64 t1 = seed_base + static_cast<i64>(min(q.m, tile * 32 + 32));
+            t0 = seed_base + static_cast<i64>(tile * 32);
+            t1 = seed_base + static_cast<i64>(min(q.m, tile * 32 + 32));
+        } else if (seed_base == kSeedSortedIdx) {
+            // ascending centre indices: seed from their window when the tile is dense along the curve
+            t0 = q.idx[tile * 32];
+            t1 = static_cast<i64>(q.idx[min(q.m, tile * 32 + 32) - 1]) + 1;
+            if (t1 - t0 > 4 * 32) t1 = -1;
+        }
+        if (t1 >= 0) {
             i64 lo = t0 - static_cast<i64>(seed_half);
             if (lo < 0) lo = 0;
             i64 hi_ = t1 + static_cast<i64>(seed_half);

@@ -49,6 +49,10 @@ void count_launch();
 inline void require(bool ok, int status, const std::string& msg) {
     if (!ok) throw Error(status, msg);
 }
+// literal messages: no std::string is built unless the check fails (hot host loops)
+inline void require(bool ok, int status, const char* msg) {
+    if (!ok) throw Error(status, msg);
+}
 
 // ---- curve tables (CurveStepper, sfc.hpp:143-164) -----------------------------------------
 // enc[s*8 + g] = (code digit c) | (next state << 3) for octant digit g = x<<2|y<<1|z;
@@ -185,6 +189,17 @@ struct Queries;
 lo_csr* radius_struct_search(lo_context* ctx, const lo_octree* t, const lo_coded* c, int shape,
                              double r, const Queries& q, bool fingerprint);
 void ensure_expanded(lo_context* ctx, lo_csr* csr);
+// centres.cu: explicit centre lists searched in curve order (sorted), rows scattered back.
+struct SortedCentres {
+    u32* idx = nullptr;  // ascending centre indices
+    u32* pos = nullptr;  // their positions in the caller's list
+};
+SortedCentres sort_centres(lo_context* ctx, const u32* centres, u64 m);
+void unsort_csr(lo_context* ctx, const SortedCentres& s, lo_csr* c);
+void unsort_knn(lo_context* ctx, const SortedCentres& s, lo_knn_result* r);
+// reorder.cu: stable LSD sort of u64 keys (passes for `level`*3 bits, constant digits skipped
+// per hist_host[8*256]); perm = original positions.
+void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int level, u64* keys_sorted, u32* perm);
 // reorder.cu: reorder_cloud over a device AoS cloud.
 lo_coded* reorder_device(lo_context* ctx, const double* xyz, u64 n, int curve, int level);
 // octree.cu: LinearOctree(LeafArray, Discretizer, Curve, n_max) over host leaf arrays.

@@ -609,8 +609,8 @@ lo_octree* octree_from_leaves(lo_context* ctx, const lo_coded* coded, const u64*
         const u64 span = b_host[i + 1] - b_host[i];
         const bool aligned_pow8 = b_host[i + 1] > b_host[i] && (span & (span - 1)) == 0 &&
                                   __builtin_ctzll(span) % 3 == 0 && b_host[i] % span == 0;
-        require(aligned_pow8 && off_host[i] <= off_host[i + 1], LO_INVALID_ARGUMENT,
-                "linear octree: misaligned leaf span at " + std::to_string(i));
+        if (!aligned_pow8 || off_host[i] > off_host[i + 1])
+            throw Error(LO_INVALID_ARGUMENT, "linear octree: misaligned leaf span at " + std::to_string(i));
     }
     // the device tree searches this cloud: its leaves must index exactly its points
     require(off_host[count - 1] == coded->n && level == coded->level && curve == coded->curve,

@@ -379,16 +379,19 @@ int lo_radius(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int
         const u64 rows = centres_host ? m : coded->n;
         ensure_float_shadows(ctx, coded, tree);
         u32* cidx = upload_centres(ctx, centres_host, m, coded->n);
-        Queries q{coded->x, coded->y, coded->z, cidx, rows, coded->pf, coded->bmax};
+        // explicit centres are searched in curve order, rows scattered back (centres.cu)
+        SortedCentres sc = sort_centres(ctx, cidx, centres_host ? m : 0);
+        Queries q{coded->x, coded->y, coded->z, centres_host ? sc.idx : nullptr, rows, coded->pf, coded->bmax};
         try {
             *out = method == LO_METHOD_STRUCT
                        ? radius_struct_search(ctx, tree, coded, shape, radius, q, fingerprint != 0)
                        : radius_search(ctx, tree, coded, shape, radius, q, fingerprint != 0);
+            if (centres_host) unsort_csr(ctx, sc, *out);
         } catch (...) {
-            dfree(ctx, cidx);
+            dfree(ctx, cidx), dfree(ctx, sc.idx), dfree(ctx, sc.pos);
             throw;
         }
-        dfree(ctx, cidx);
+        dfree(ctx, cidx), dfree(ctx, sc.idx), dfree(ctx, sc.pos);
     });
 }
 

@@ -397,7 +397,7 @@ static EncodeParams make_params(const double box[6], const double scale[3], int 
 }
 
 // Sorts (codes, implicit original index) stably; writes sorted keys + perm.
-static void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int level,
+void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int level,
                        u64* keys_sorted, u32* perm) {
     const int passes = (3 * level + 7) / 8;
     // digit bases per pass and the constant-digit skip (reorder.cpp:49)
