@@ -192,10 +192,34 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
             t0 = seed_base + static_cast<i64>(tile * 32);
             t1 = seed_base + static_cast<i64>(min(q.m, tile * 32 + 32));
         } else if (seed_base == kSeedSortedIdx) {
-            // ascending centre indices: seed from their window when the tile is dense along the curve
+            // ascending centre indices: seed from their window when the tile is dense along the
+            // curve; a sparse tile (random subset) seeds every lane from its own centre's window
             t0 = q.idx[tile * 32];
             t1 = static_cast<i64>(q.idx[min(q.m, tile * 32 + 32) - 1]) + 1;
-            if (t1 - t0 > 4 * 32) t1 = -1;
+            if (t1 - t0 > 4 * 32) {
+                t1 = -1;
+                if (active) {
+                    const i64 c = q.idx[qi];
+                    i64 lo = c - static_cast<i64>(seed_half / 2);
+                    if (lo < 0) lo = 0;
+                    i64 hi_ = lo + static_cast<i64>(seed_half);
+                    if (hi_ > static_cast<i64>(npoints)) {
+                        hi_ = static_cast<i64>(npoints);
+                        lo = hi_ - static_cast<i64>(seed_half) < 0 ? 0 : hi_ - static_cast<i64>(seed_half);
+                    }
+                    skip_lo = static_cast<u32>(lo);
+                    skip_hi = static_cast<u32>(hi_);
+                    for (u32 g = skip_lo; g < skip_hi; ++g) {
+                        const float4 p = __ldg(pf + g);
+                        const float dx = p.x - qf.x, dy = p.y - qf.y, dz = p.z - qf.z;
+                        const float v = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                        if (v <= T) {
+                            const double pd[3] = {__ldg(px + g), __ldg(py + g), __ldg(pz + g)};
+                            knn_offer(heap, k, worst_d, worst_i, T, E, v, g, cx, cy, cz, pd);
+                        }
+                    }
+                }
+            }
         }
         if (t1 >= 0) {
             i64 lo = t0 - static_cast<i64>(seed_half);
@@ -245,7 +269,7 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
                 continue;
             }
             // leaf: skip if no lane's threshold reaches it, or it lies inside the seed window
-            if (nd.begin >= skip_lo && nd.end <= skip_hi) continue;
+            if (__all_sync(~0u, nd.begin >= skip_lo && nd.end <= skip_hi)) continue;  // seeded already
             bool want = false;
             if (active) {
                 const float nx = fmaxf(fmaxf(nd.lo[0] - qf.x, qf.x - nd.hi[0]), 0.f);
