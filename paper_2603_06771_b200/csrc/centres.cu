@@ -199,4 +199,26 @@ void unsort_csr(lo_context* ctx, const SortedCentres& s, lo_csr* c) {
     sync(ctx);
 }
 
+__global__ void gather_q(const u32* __restrict__ pos, u64 m, const double* __restrict__ x,
+                         const double* __restrict__ y, const double* __restrict__ z, const float4* __restrict__ f,
+                         double* __restrict__ x2, double* __restrict__ y2, double* __restrict__ z2,
+                         float4* __restrict__ f2) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
+        const u32 j = pos[i];
+        x2[i] = x[j], y2[i] = y[j], z2[i] = z[j], f2[i] = f[j];
+    }
+}
+
+void gather_queries(lo_context* ctx, const u32* pos, u64 m, double*& x, double*& y, double*& z, float4*& f) {
+    if (m == 0) return;
+    double* x2 = dalloc_t<double>(ctx, m);
+    double* y2 = dalloc_t<double>(ctx, m);
+    double* z2 = dalloc_t<double>(ctx, m);
+    float4* f2 = dalloc_t<float4>(ctx, m);
+    gather_q<<<grid_n(ctx, m), 256, 0, ctx->stream>>>(pos, m, x, y, z, f, x2, y2, z2, f2);
+    LO_CHECK_LAUNCH();
+    dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f);
+    x = x2, y = y2, z = z2, f = f2;
+}
+
 }  // namespace lo

@@ -200,6 +200,11 @@ void unsort_knn(lo_context* ctx, const SortedCentres& s, lo_knn_result* r);
 // reorder.cu: stable LSD sort of u64 keys (passes for `level`*3 bits, constant digits skipped
 // per hist_host[8*256]); perm = original positions.
 void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int level, u64* keys_sorted, u32* perm);
+// reorder.cu: positions of arbitrary query points (SoA, device) in curve order.
+u32* sort_points_sfc(lo_context* ctx, const lo_coded* c, const double* x, const double* y, const double* z,
+                     u64 m);
+// centres.cu: gather query arrays (x, y, z, f) into curve order in place.
+void gather_queries(lo_context* ctx, const u32* pos, u64 m, double*& x, double*& y, double*& z, float4*& f);
 // reorder.cu: reorder_cloud over a device AoS cloud.
 lo_coded* reorder_device(lo_context* ctx, const double* xyz, u64 n, int curve, int level);
 // octree.cu: LinearOctree(LeafArray, Discretizer, Curve, n_max) over host leaf arrays.

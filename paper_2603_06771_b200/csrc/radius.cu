@@ -403,14 +403,19 @@ int lo_radius_points(lo_context* ctx, const lo_octree* tree, const lo_coded* cod
         double *x = nullptr, *y = nullptr, *z = nullptr, bmax = 0.0;
         float4* f = nullptr;
         if (m) upload_points(ctx, coded, queries_host, m, &x, &y, &z, &f, &bmax);
-        Queries q{x, y, z, nullptr, m, f, bmax};
+        SortedCentres sc;
         try {
+            // search in curve order (warp tiles of spatial neighbours), rows scattered back
+            sc.pos = sort_points_sfc(ctx, coded, x, y, z, m);
+            gather_queries(ctx, sc.pos, m, x, y, z, f);
+            Queries q{x, y, z, nullptr, m, f, bmax};
             *out = radius_search(ctx, tree, coded, shape, radius, q, true);
+            unsort_csr(ctx, sc, *out);
         } catch (...) {
-            dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f);
+            dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f), dfree(ctx, sc.pos);
             throw;
         }
-        dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f);
+        dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f), dfree(ctx, sc.pos);
     });
 }
 
@@ -421,14 +426,18 @@ int lo_radius_struct_points(lo_context* ctx, const lo_octree* tree, const lo_cod
         double *x = nullptr, *y = nullptr, *z = nullptr, bmax = 0.0;
         float4* f = nullptr;
         if (m) upload_points(ctx, coded, queries_host, m, &x, &y, &z, &f, &bmax);
-        Queries q{x, y, z, nullptr, m, f, bmax};
+        SortedCentres sc;
         try {
+            sc.pos = sort_points_sfc(ctx, coded, x, y, z, m);
+            gather_queries(ctx, sc.pos, m, x, y, z, f);
+            Queries q{x, y, z, nullptr, m, f, bmax};
             *out = radius_struct_search(ctx, tree, coded, shape, radius, q, true);
+            unsort_csr(ctx, sc, *out);
         } catch (...) {
-            dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f);
+            dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f), dfree(ctx, sc.pos);
             throw;
         }
-        dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f);
+        dfree(ctx, x), dfree(ctx, y), dfree(ctx, z), dfree(ctx, f), dfree(ctx, sc.pos);
     });
 }
 

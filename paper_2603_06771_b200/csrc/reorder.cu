@@ -467,6 +467,58 @@ void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int lev
     dfree(ctx, vtmp);
 }
 
+// Curve order of arbitrary query points (clamped into the cloud's grid, so points outside the
+// cube still get a position): codes + digit histograms, then the stable radix sort.
+__global__ void __launch_bounds__(256) query_codes(const double* __restrict__ x, const double* __restrict__ y,
+                                                   const double* __restrict__ z, u64 n, EncodeParams p,
+                                                   u64* __restrict__ codes, u32* __restrict__ hist) {
+    __shared__ u8 enc[32 * 8];
+    __shared__ u32 h[8 * 256];
+    for (int i = threadIdx.x; i < 32 * 8; i += blockDim.x) enc[i] = p.enc[i];
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u32 cx = axis_cell(x[i], p.lo[0], p.scale[0], p.top);
+        const u32 cy = axis_cell(y[i], p.lo[1], p.scale[1], p.top);
+        const u32 cz = axis_cell(z[i], p.lo[2], p.scale[2], p.top);
+        const u64 code = encode_cell(cx, cy, cz, p.level, p.curve, enc);
+        codes[i] = code;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) atomicAdd(&h[b * 256 + ((code >> (8 * b)) & 0xff)], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+u32* sort_points_sfc(lo_context* ctx, const lo_coded* c, const double* x, const double* y, const double* z,
+                     u64 m) {
+    if (m == 0) return nullptr;
+    u64* codes = dalloc_t<u64>(ctx, m);
+    u64* sorted = nullptr;
+    u32* hist = nullptr;
+    u32* pos = nullptr;
+    try {
+        sorted = dalloc_t<u64>(ctx, m);
+        hist = dalloc_t<u32>(ctx, 8 * 256);
+        pos = dalloc_t<u32>(ctx, m);
+        LO_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
+        const EncodeParams p = make_params(c->disc_box, c->scale, c->level, c->curve);
+        query_codes<<<std::min(grid_for(ctx, m, 256), ctx->sm_count * 4), 256, 0, ctx->stream>>>(x, y, z, m, p,
+                                                                                              codes, hist);
+        LO_CHECK_LAUNCH();
+        std::vector<u32> hh(8 * 256);
+        LO_CUDA(cudaMemcpyAsync(hh.data(), hist, 8 * 256 * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        radix_sort(ctx, codes, m, hh.data(), c->level, sorted, pos);
+    } catch (...) {
+        dfree(ctx, codes), dfree(ctx, sorted), dfree(ctx, hist), dfree(ctx, pos);
+        throw;
+    }
+    dfree(ctx, codes), dfree(ctx, sorted), dfree(ctx, hist);
+    return pos;
+}
+
 lo_coded* reorder_device(lo_context* ctx, const double* xyz, u64 n, int curve, int level) {
     require(n > 0, LO_INVALID_ARGUMENT, "reorder_cloud: empty cloud");
     require(n <= 0xffffffffull, LO_INVALID_ARGUMENT,
