@@ -260,7 +260,11 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
                 1, std::min<u64>((tiles + kReplayWarps - 1) / kReplayWarps, ctx->sm_count * 16ull)));
             // short rows: buffer-major stores stay line-local; long rows: row-major so every
             // output line completes while hot (measured crossover ~ 64 members per row)
-            if (out->total < 64ull * q.m)
+            static const u64 row_major_min = [] {  // mean row length from which rows go row-major
+                const char* e = std::getenv("LO_REPLAY_ROW_MAJOR_MIN");
+                return e ? std::strtoull(e, nullptr, 10) : 96ull;
+            }();
+            if (out->total < row_major_min * q.m)
                 radius_replay_bm_kernel<<<rb, 128, 0, ctx->stream>>>(ra.rp, q.m, out->offsets, out->indices,
                                                                     ovf, ovf_n);
             else {
