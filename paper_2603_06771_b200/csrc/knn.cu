@@ -45,6 +45,35 @@ struct LaneHeap {
         hi[pos * 32] = i;
     }
 
+    // sift_down for a compile-time n = 2^LOGK: at most LOGK levels, fully unrolled
+    template <int LOGK>
+    __device__ __forceinline__ void sift_down_fixed(double d, u32 i) {
+        constexpr u32 n = 1u << LOGK;
+        u32 pos = 0;
+#pragma unroll
+        for (int lv = 0; lv < LOGK; ++lv) {
+            u32 c = 2 * pos + 1;
+            if (c >= n) break;
+            double cd = hd[c * 32];
+            u32 ci = hi[c * 32];
+            if (c + 1 < n) {
+                const double rd = hd[(c + 1) * 32];
+                const u32 ri = hi[(c + 1) * 32];
+                if (after(rd, ri, cd, ci)) {
+                    c = c + 1;
+                    cd = rd;
+                    ci = ri;
+                }
+            }
+            if (!after(cd, ci, d, i)) break;
+            hd[pos * 32] = cd;
+            hi[pos * 32] = ci;
+            pos = c;
+        }
+        hd[pos * 32] = d;
+        hi[pos * 32] = i;
+    }
+
     // replace the maximum and restore the heap over [0, n)
     __device__ __forceinline__ void sift_down(double d, u32 i, u32 n) {
         u32 pos = 0;
@@ -330,17 +359,29 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
             if (global_heap) {
                 gd = dalloc_t<double>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
                 gi = dalloc_t<u32>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
-                LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<true>,
+                LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<true, 0>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                knn_float_kernel<true><<<blocks, 32 * warps, smem, ctx->stream>>>(
+                knn_float_kernel<true, 0><<<blocks, 32 * warps, smem, ctx->stream>>>(
                     t->tf, c->pf, c->x, c->y, c->z, c->n, q, seed_base, seed_half, E, kh, out->idx,
                     out->dist, gd, gi, counter);
             } else {
-                LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                knn_float_kernel<false><<<blocks, 32 * warps, smem, ctx->stream>>>(
-                    t->tf, c->pf, c->x, c->y, c->z, c->n, q, seed_base, seed_half, E, kh, out->idx,
-                    out->dist, nullptr, nullptr, counter);
+                // common k compile to fixed-depth, unrolled heap sifts
+#define LO_KNN_LAUNCH(KC)                                                                                 \
+    do {                                                                                                  \
+        LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<false, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     static_cast<int>(smem)));                                            \
+        knn_float_kernel<false, KC><<<blocks, 32 * warps, smem, ctx->stream>>>(                           \
+            t->tf, c->pf, c->x, c->y, c->z, c->n, q, seed_base, seed_half, E, kh, out->idx, out->dist,    \
+            nullptr, nullptr, counter);                                                                   \
+    } while (0)
+                switch (kh) {
+                    case 8: LO_KNN_LAUNCH(8); break;
+                    case 16: LO_KNN_LAUNCH(16); break;
+                    case 32: LO_KNN_LAUNCH(32); break;
+                    case 64: LO_KNN_LAUNCH(64); break;
+                    default: LO_KNN_LAUNCH(0); break;
+                }
+#undef LO_KNN_LAUNCH
             }
             LO_CHECK_LAUNCH();
             dfree(ctx, counter);

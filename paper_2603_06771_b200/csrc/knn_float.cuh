@@ -54,6 +54,7 @@ __device__ __forceinline__ float knn_threshold(double w, float E) {
 }
 
 // One candidate j (global index g, FP32 squared distance v) for this lane.
+template <int KC>
 __device__ __forceinline__ void knn_offer(LaneHeap& heap, u32 k, double& worst_d, u32& worst_i,
                                           float& T, float E, float v, u32 g, double cx, double cy,
                                           double cz, const double* pxyz) {
@@ -67,7 +68,11 @@ __device__ __forceinline__ void knn_offer(LaneHeap& heap, u32 k, double& worst_d
             T = knn_threshold(worst_d, E);
         }
     } else if (after(worst_d, worst_i, d, g)) {
-        heap.sift_down(d, g, k);
+        if constexpr (KC == 8) heap.sift_down_fixed<3>(d, g);
+        else if constexpr (KC == 16) heap.sift_down_fixed<4>(d, g);
+        else if constexpr (KC == 32) heap.sift_down_fixed<5>(d, g);
+        else if constexpr (KC == 64) heap.sift_down_fixed<6>(d, g);
+        else heap.sift_down(d, g, k);
         worst_d = heap.hd[0];
         worst_i = heap.hi[0];
         T = knn_threshold(worst_d, E);
@@ -75,6 +80,7 @@ __device__ __forceinline__ void knn_offer(LaneHeap& heap, u32 k, double& worst_d
 }
 
 // Tests the `cnt` staged candidates against this lane's query (pairs, packed FP32).
+template <int KC>
 __device__ __forceinline__ void knn_chunk(const KnnSmem& S, u32 cnt, bool active, u64 QX, u64 QY,
                                           u64 QZ, LaneHeap& heap, u32 k, double& worst_d,
                                           u32& worst_i, float& T, float E, double cx, double cy,
@@ -95,12 +101,12 @@ __device__ __forceinline__ void knn_chunk(const KnnSmem& S, u32 cnt, bool active
         if (v0 <= T) {
             const u32 g = S.pidx[2 * pp];
             if (g < skip_lo || g >= skip_hi)
-                knn_offer(heap, k, worst_d, worst_i, T, E, v0, g, cx, cy, cz, S.pd + 6 * pp);
+                knn_offer<KC>(heap, k, worst_d, worst_i, T, E, v0, g, cx, cy, cz, S.pd + 6 * pp);
         }
         if (2 * pp + 1 < cnt && v1 <= T) {
             const u32 g = S.pidx[2 * pp + 1];
             if (g < skip_lo || g >= skip_hi)
-                knn_offer(heap, k, worst_d, worst_i, T, E, v1, g, cx, cy, cz, S.pd + 6 * pp + 3);
+                knn_offer<KC>(heap, k, worst_d, worst_i, T, E, v1, g, cx, cy, cz, S.pd + 6 * pp + 3);
         }
     }
 }
@@ -131,14 +137,15 @@ __device__ __forceinline__ void knn_stage(const KnnSmem& S, const float4* __rest
 constexpr int kKnnFloatStack = kStackCap;
 constexpr i64 kSeedSortedIdx = -2;  // seed_base: queries are ascending cloud indices (q.idx)
 
-template <bool GLOBAL_HEAP>
+template <bool GLOBAL_HEAP, int KC>
 __global__ void __launch_bounds__(128) knn_float_kernel(
     const TNodeF* __restrict__ tf, const float4* __restrict__ pf, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, u64 npoints, Queries q,
-    i64 seed_base, u32 seed_half, float E, u32 k, u32* __restrict__ out_idx,
+    i64 seed_base, u32 seed_half, float E, u32 k_in, u32* __restrict__ out_idx,
     double* __restrict__ out_dist, double* __restrict__ gheap_d, u32* __restrict__ gheap_i,
     u64* tile_counter) {
     extern __shared__ __align__(16) unsigned char smem[];
+    const u32 k = KC > 0 ? static_cast<u32>(KC) : k_in;
     const int warps = blockDim.x >> 5;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned char* mine = smem + w * kKnnFixed;
@@ -215,7 +222,7 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
                         const float v = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
                         if (v <= T) {
                             const double pd[3] = {__ldg(px + g), __ldg(py + g), __ldg(pz + g)};
-                            knn_offer(heap, k, worst_d, worst_i, T, E, v, g, cx, cy, cz, pd);
+                            knn_offer<KC>(heap, k, worst_d, worst_i, T, E, v, g, cx, cy, cz, pd);
                         }
                     }
                 }
@@ -231,7 +238,7 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
             for (u32 b = skip_lo; b < skip_hi; b += 32) {
                 const u32 cnt = min(32u, skip_hi - b);
                 knn_stage(S, pf, px, py, pz, b, cnt, lane);
-                knn_chunk(S, cnt, active, QX, QY, QZ, heap, k, worst_d, worst_i, T, E, cx, cy, cz,
+                knn_chunk<KC>(S, cnt, active, QX, QY, QZ, heap, k, worst_d, worst_i, T, E, cx, cy, cz,
                           0u, 0u);
             }
         }
@@ -281,7 +288,7 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
             for (u32 b = nd.begin; b < nd.end; b += 32) {
                 const u32 cnt = min(32u, nd.end - b);
                 knn_stage(S, pf, px, py, pz, b, cnt, lane);
-                knn_chunk(S, cnt, want, QX, QY, QZ, heap, k, worst_d, worst_i, T, E, cx, cy, cz,
+                knn_chunk<KC>(S, cnt, want, QX, QY, QZ, heap, k, worst_d, worst_i, T, E, cx, cy, cz,
                           skip_lo, skip_hi);
             }
         }
