@@ -150,6 +150,7 @@ struct lo_octree {
     lo::TNode* tn = nullptr;            // [tnodes]
     lo::TNodeF* tf = nullptr;           // [tnodes] FP32 shadow (built lazily for replicas)
     double* rb = nullptr;               // [tnodes*6] padded octant boxes (Struct; built lazily)
+    float4* rbf = nullptr;              // [tnodes*2] the same, FP32 outward-rounded, relative to origin
     int max_depth = 0;
 };
 

@@ -357,9 +357,27 @@ __global__ void tnode_ref_boxes(const TNode* __restrict__ tn, const u8* __restri
     }
 }
 
+// FP32 copies of the reference boxes for the filtered Struct relation: outward-rounded, relative
+// to the cloud origin like the point filter copies.
+__global__ void ref_boxes_float(const double* __restrict__ rb, u64 count, double ox, double oy, double oz,
+                                float4* __restrict__ rbf) {
+    for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < count; t += (u64)gridDim.x * blockDim.x) {
+        const double* b = rb + 6 * t;
+        const double o[3] = {ox, oy, oz};
+        float lo[3], hi[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = __double2float_rd(__dsub_rd(b[a], o[a]));
+            hi[a] = __double2float_ru(__dsub_ru(b[3 + a], o[a]));
+        }
+        rbf[2 * t] = make_float4(lo[0], lo[1], lo[2], 0.f);
+        rbf[2 * t + 1] = make_float4(hi[0], hi[1], hi[2], 0.f);
+    }
+}
+
 void ensure_ref_boxes(lo_context* ctx, const lo_coded* coded, const lo_octree* tree) {
     auto* t = const_cast<lo_octree*>(tree);
-    if (t->rb) return;
+    if (t->rb && t->rbf) return;
     const u64 T = t->tnodes;
     u8* depth = dalloc_t<u8>(ctx, T);
     double* rb = nullptr;
@@ -378,9 +396,15 @@ void ensure_ref_boxes(lo_context* ctx, const lo_coded* coded, const lo_octree* t
         std::memcpy(p.dec, curve_tables(t->curve).dec, sizeof p.dec);
         tnode_ref_boxes<<<g, 256, 0, ctx->stream>>>(t->tn, depth, T, coded->codes, p, rb);
         LO_CHECK_LAUNCH();
+        t->rbf = dalloc_t<float4>(ctx, 2 * T);
+        ref_boxes_float<<<g, 256, 0, ctx->stream>>>(rb, T, coded->origin[0], coded->origin[1], coded->origin[2],
+                                                    t->rbf);
+        LO_CHECK_LAUNCH();
     } catch (...) {
         dfree(ctx, depth);
         dfree(ctx, rb);
+        dfree(ctx, t->rbf);
+        t->rbf = nullptr;
         throw;
     }
     dfree(ctx, depth);
@@ -797,6 +821,7 @@ int lo_octree_destroy(lo_octree* t) {
         dfree(ctx, t->tn);
         dfree(ctx, t->tf);
         dfree(ctx, t->rb);
+        dfree(ctx, t->rbf);
         delete t;
     });
 }

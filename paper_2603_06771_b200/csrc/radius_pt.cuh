@@ -184,7 +184,7 @@ constexpr int kReplayWarps = 4;
 
 // Buffer-major replay for short rows (small radii): per record, one coalesced store per query
 // with members; the few, short rows of a tile stay within a handful of lines.
-__global__ void __launch_bounds__(128) radius_replay_bm_kernel(
+static __global__ void __launch_bounds__(128) radius_replay_bm_kernel(
     RecPool rp, u64 m, const u64* __restrict__ offsets, u32* __restrict__ out,
     u32* __restrict__ overflow_list, u32* __restrict__ overflow_n) {
     const int lane = threadIdx.x & 31;
@@ -227,7 +227,7 @@ constexpr u32 kReplayMaskStride = 33;
 constexpr size_t kReplayWarpWords = 32 * 32 + 32 * kReplayMaskStride;
 constexpr size_t kReplaySmem = kReplayWarps * kReplayWarpWords * 4;
 
-__global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_kernel(
+static __global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_kernel(
     RecPool rp, u64 m, const u64* __restrict__ offsets, u32* __restrict__ out,
     u32* __restrict__ overflow_list, u32* __restrict__ overflow_n) {
     extern __shared__ __align__(16) u32 replay_smem[];

@@ -16,9 +16,265 @@
 // hashed like search.cpp:325-336.
 #include <algorithm>
 
-#include "radius_float.cuh"
+#include "radius_pt.cuh"
 
 namespace lo {
+
+// ---- fast path: the lin count kernel's lane = point buffers + the FP32 filter ----------------
+// Node relations against the reference's octant boxes are decided in FP32 on outward-rounded
+// copies of those boxes (rbf) with the FloatTest margins -- Contains iff far^2 < t_lo, not
+// Contains iff far^2 >= t_hi, Disjoint iff near^2 >= t_hi, not Disjoint iff near^2 < t_lo -- and
+// only the band in between is evaluated in FP64 on the exact boxes (rb).  Leaf points go through
+// the 32-slot buffers; each slot carries the mask of queries that reached its leaf as Intersects,
+// so a query that contains (or skipped) that leaf never counts its points as singles.
+enum { kRelU = 3 };  // "uncertain": decide in FP64
+
+template <int SHAPE>
+__device__ __forceinline__ int classify_ref_f(const float4& q, const float4& lo, const float4& hi,
+                                              const FloatTest& ft) {
+    const float nx = fmaxf(fmaxf(lo.x - q.x, q.x - hi.x), 0.f);
+    const float ny = fmaxf(fmaxf(lo.y - q.y, q.y - hi.y), 0.f);
+    const float fx = fmaxf(q.x - lo.x, hi.x - q.x);
+    const float fy = fmaxf(q.y - lo.y, hi.y - q.y);
+    float nm, fm, tl, th;
+    if (SHAPE == LO_SPHERE || SHAPE == LO_CUBE) {
+        const float nz = fmaxf(fmaxf(lo.z - q.z, q.z - hi.z), 0.f);
+        const float fz = fmaxf(q.z - lo.z, hi.z - q.z);
+        if (SHAPE == LO_SPHERE) {
+            nm = fmaf(nz, nz, fmaf(ny, ny, nx * nx));
+            fm = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
+            tl = ft.t_lo, th = ft.t_hi;
+        } else {
+            nm = fmaxf(fmaxf(nx, ny), nz);
+            fm = fmaxf(fmaxf(fx, fy), fz);
+            tl = ft.r_lo, th = ft.r_hi;
+        }
+    } else if (SHAPE == LO_CIRCLE) {
+        nm = fmaf(ny, ny, nx * nx);
+        fm = fmaf(fy, fy, fx * fx);
+        tl = ft.t_lo, th = ft.t_hi;
+    } else {
+        nm = fmaxf(nx, ny);
+        fm = fmaxf(fx, fy);
+        tl = ft.r_lo, th = ft.r_hi;
+    }
+    if (fm < tl) return kContains;
+    if (fm < th) return kRelU;
+    if (nm >= th) return kDisjoint;
+    if (nm >= tl) return kRelU;
+    return kIntersects;
+}
+
+struct StructShared {
+    PtShared pt;
+    u32 sw[32];  // per buffer slot: queries that reached the slot's leaf as Intersects
+};
+
+// Tests the buffer (lane j = slot j) against every query whose bit is in qmask; a query counts a
+// slot only if the slot's want mask holds it.  Count pass: lane L adds its members to `ns`;
+// fill pass: members of query L go to srow_base + cursor (coalesced per query).
+template <int SHAPE, bool FILL>
+__device__ __forceinline__ void struct_buffer(StructShared& SS, u32 qmask, int lane, float lo_thr,
+                                              float hi_thr, const double* __restrict__ px,
+                                              const double* __restrict__ py, const double* __restrict__ pz,
+                                              double r, double r2, u32* __restrict__ singles, u64 srow,
+                                              u32& ns) {
+    PtShared& S = SS.pt;
+    const float4 P = S.buf[lane];
+    const u32 idx = __float_as_uint(P.w);
+    const u32 sw = SS.sw[lane];
+    const u32 lt = (1u << lane) - 1u;
+    u32 pm = (qmask | (qmask >> 1)) & 0x55555555u;
+    while (pm) {
+        const int b = __ffs(pm) - 1;
+        pm &= pm - 1;
+        float v0, v1;
+        if (SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE) {
+            const u64 PX = pack2(P.x, P.x), PY = pack2(P.y, P.y);
+            const u64 dx = fsub2(PX, *reinterpret_cast<const u64*>(&S.qx[b]));
+            const u64 dy = fsub2(PY, *reinterpret_cast<const u64*>(&S.qy[b]));
+            u64 d2 = fmul2(dx, dx);
+            d2 = ffma2(dy, dy, d2);
+            if (SHAPE == LO_SPHERE) {
+                const u64 dz = fsub2(pack2(P.z, P.z), *reinterpret_cast<const u64*>(&S.qz[b]));
+                d2 = ffma2(dz, dz, d2);
+            }
+            unpack2(d2, v0, v1);
+        } else {
+            v0 = metric_f<SHAPE>(S.qf[b], P);
+            v1 = metric_f<SHAPE>(S.qf[b + 1], P);
+        }
+        const bool w0 = (sw >> b) & 1u, w1 = (sw >> (b + 1)) & 1u;
+        u32 in0 = __ballot_sync(~0u, w0 && v0 < lo_thr);
+        u32 in1 = __ballot_sync(~0u, w1 && v1 < lo_thr);
+        const u32 h0 = __ballot_sync(~0u, w0 && v0 < hi_thr);
+        const u32 h1 = __ballot_sync(~0u, w1 && v1 < hi_thr);
+        if (h0 ^ in0) in0 = band_fix<SHAPE>(in0, h0 ^ in0, S, b, lane, idx, px, py, pz, r, r2);
+        if (h1 ^ in1) in1 = band_fix<SHAPE>(in1, h1 ^ in1, S, b + 1, lane, idx, px, py, pz, r, r2);
+        if (FILL) {
+            const u32 c0 = __shfl_sync(~0u, ns, b);
+            const u32 c1 = __shfl_sync(~0u, ns, b + 1);
+            const u64 s0 = __shfl_sync(~0u, srow, b);
+            const u64 s1 = __shfl_sync(~0u, srow, b + 1);
+            if ((in0 >> lane) & 1u) singles[s0 + c0 + __popc(in0 & lt)] = idx;
+            if ((in1 >> lane) & 1u) singles[s1 + c1 + __popc(in1 & lt)] = idx;
+        }
+        ns += lane == b ? __popc(in0) : (lane == b + 1 ? __popc(in1) : 0u);
+    }
+}
+
+template <int SHAPE, bool FILL>
+__global__ void __launch_bounds__(kPtThreads, 8) struct_pt_kernel(
+    const TNodeF* __restrict__ tf, const float4* __restrict__ rbf, const double* __restrict__ rb,
+    const float4* __restrict__ pf, const double* __restrict__ px, const double* __restrict__ py,
+    const double* __restrict__ pz, Queries q, FloatTest ft, float compact, double r, double r2,
+    u32* __restrict__ counts, u32* __restrict__ nrng, u32* __restrict__ nsgl,
+    const u64* __restrict__ r_off, u32* __restrict__ ranges, const u64* __restrict__ s_off,
+    u32* __restrict__ singles, u64* tile_counter) {
+    __shared__ StructShared shared_s[kPtWarps];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    StructShared& SS = shared_s[w];
+    PtShared& S = SS.pt;
+    const u64 ntiles = (q.m + 31) / 32;
+    const int cl = lane & 7, grp = lane >> 3;
+    constexpr bool kSq = SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE;
+    const float lo_thr = kSq ? ft.t_lo : ft.r_lo;
+    const float hi_thr = kSq ? ft.t_hi : ft.r_hi;
+    for (;;) {
+        u64 tile = 0;
+        if (lane == 0) tile = atomicAdd(reinterpret_cast<unsigned long long*>(tile_counter), 1ull);
+        tile = __shfl_sync(~0u, tile, 0);
+        if (tile >= ntiles) break;
+        const u64 qi = tile * 32 + lane;
+        const bool active = qi < q.m;
+        double cx = 0.0, cy = 0.0, cz = 0.0;
+        float4 qf = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+        if (active) {
+            load_query(q, qi, cx, cy, cz);
+            qf = load_query_f(q, qi);
+        }
+        __syncwarp();
+        S.qf[lane] = qf;
+        S.qx[lane] = qf.x;
+        S.qy[lane] = qf.y;
+        S.qz[lane] = qf.z;
+        S.qd[lane][0] = cx;
+        S.qd[lane][1] = cy;
+        S.qd[lane][2] = cz;
+        u32 count = 0, nr = 0, ns = 0, last_e = 0, skip_end = 0;
+        u32* rrow = nullptr;
+        u64 srow = 0;
+        if (FILL && active) {
+            rrow = ranges + 2 * r_off[qi];
+            srow = s_off[qi];
+        }
+        float gl[3] = {qf.x, qf.y, qf.z}, gh[3] = {qf.x, qf.y, qf.z};
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                gl[a] = fminf(gl[a], __shfl_xor_sync(~0u, gl[a], o));
+                gh[a] = fmaxf(gh[a], __shfl_xor_sync(~0u, gh[a], o));
+            }
+        }
+        const bool gcompact = fmaxf(fmaxf(gh[0] - gl[0], gh[1] - gl[1]), gh[2] - gl[2]) <= compact;
+        u32 fill = 0, qmask = 0;
+        auto flush = [&]() {
+            struct_buffer<SHAPE, FILL>(SS, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2, singles, srow, ns);
+        };
+        int sp = 1;
+        if (lane == 0) S.stack[0] = 0;
+        __syncwarp();
+        while (sp > 0) {
+            const u32 t = S.stack[--sp];
+            const NodeF nd = load_node_f(tf, t);
+            // this lane's relation to the node's reference octant box
+            int rel = kDisjoint;
+            const bool live = active && nd.begin >= skip_end;
+            if (live) {
+                const float4 blo = __ldg(rbf + 2 * static_cast<u64>(t));
+                const float4 bhi = __ldg(rbf + 2 * static_cast<u64>(t) + 1);
+                rel = classify_ref_f<SHAPE>(qf, blo, bhi, ft);
+                if (rel == kRelU) {
+                    NodeView box;
+                    const double* bb = rb + 6 * static_cast<u64>(t);
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) box.lo[a] = __ldg(bb + a), box.hi[a] = __ldg(bb + 3 + a);
+                    rel = relation<SHAPE>(cx, cy, cz, r, r2, box);
+                }
+                if (rel == kContains) {
+                    if (nr > 0 && last_e == nd.begin) {
+                        if (FILL) rrow[2 * (nr - 1) + 1] = nd.end;
+                    } else {
+                        if (FILL) rrow[2 * nr] = nd.begin, rrow[2 * nr + 1] = nd.end;
+                        ++nr;
+                    }
+                    last_e = nd.end;
+                    count += nd.end - nd.begin;
+                }
+                if (rel != kIntersects) skip_end = nd.end;  // Contains / Disjoint: not descended
+            }
+            const u32 inter = __ballot_sync(~0u, rel == kIntersects);
+            if (!inter) continue;
+            if (nd.nchild != 0) {
+                bool keep = false;
+                if (cl < static_cast<int>(nd.nchild)) {
+                    const NodeF ch = load_node_f(tf, nd.child0 + cl);
+                    if (gcompact) {
+                        keep = !tile_disjoint_f<SHAPE>(gl, gh, ch, ft);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) keep |= !disjoint_f<SHAPE>(S.qf[8 * grp + j], ch, ft);
+                    }
+                }
+                u32 sb = __ballot_sync(~0u, keep);
+                sb = (sb | (sb >> 8) | (sb >> 16) | (sb >> 24)) & 0xffu;
+                const int k = __popc(sb);
+                __syncwarp();
+                if (lane < 8 && ((sb >> lane) & 1u))
+                    S.stack[sp + k - 1 - __popc(sb & ((1u << lane) - 1u))] = nd.child0 + lane;
+                sp += k;
+                __syncwarp();
+                continue;
+            }
+            // leaf: its points, wanted by the lanes that found it Intersects
+            for (u32 base = nd.begin; base < nd.end;) {
+                const u32 take = min(32u - fill, nd.end - base);
+                __syncwarp();
+                if (static_cast<u32>(lane) < take) {
+                    float4 p = __ldg(pf + base + lane);
+                    p.w = __uint_as_float(base + lane);
+                    S.buf[fill + lane] = p;
+                    SS.sw[fill + lane] = inter;
+                }
+                fill += take;
+                qmask |= inter;
+                base += take;
+                if (fill == 32) {
+                    __syncwarp();
+                    flush();
+                    fill = 0;
+                    qmask = 0;
+                }
+            }
+        }
+        if (fill) {
+            __syncwarp();
+            if (static_cast<u32>(lane) >= fill) {
+                S.buf[lane] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+                SS.sw[lane] = 0;
+            }
+            __syncwarp();
+            flush();
+        }
+        if (!FILL && active) {
+            counts[qi] = count + ns;
+            nrng[qi] = nr;
+            nsgl[qi] = ns;
+        }
+        __syncwarp();
+    }
+}
 
 template <int SHAPE, bool FILL>
 __global__ void __launch_bounds__(kRadiusThreads) radius_struct_kernel(
@@ -155,6 +411,31 @@ static void launch_struct(lo_context* ctx, int shape, const lo_octree* t, const 
                           const Queries& q, double r, lo_csr* out, u32* nrng, u32* nsgl) {
     const double r2 = r * r;  // SearchKernel ctor (geometry.hpp:107)
     const u64 tiles = (q.m + 31) / 32;
+    const FloatTest ft = make_float_test(r, std::max(c->bmax, q.bmax));
+    if (ft.enabled && q.f && t->tf && c->pf && t->rbf) {
+        u64* counter = dalloc_t<u64>(ctx, 1);
+        LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
+        const int pblocks = static_cast<int>(std::max<u64>(
+            1, std::min<u64>((tiles + kPtWarps - 1) / kPtWarps, static_cast<u64>(ctx->sm_count) * 8)));
+        const float compact = static_cast<float>(4.0 * r);
+#define LO_STRUCT_PT(S)                                                                              \
+    case S:                                                                                          \
+        struct_pt_kernel<S, FILL><<<pblocks, kPtThreads, 0, ctx->stream>>>(                          \
+            t->tf, t->rbf, t->rb, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, out->counts, nrng,  \
+            nsgl, out->range_offsets, out->ranges, out->single_offsets, out->singles, counter);      \
+        break;
+        switch (shape) {
+            LO_STRUCT_PT(LO_SPHERE)
+            LO_STRUCT_PT(LO_CIRCLE)
+            LO_STRUCT_PT(LO_CUBE)
+            LO_STRUCT_PT(LO_SQUARE)
+            default: throw Error(LO_INVALID_ARGUMENT, "unknown kernel shape");
+        }
+#undef LO_STRUCT_PT
+        LO_CHECK_LAUNCH();
+        dfree(ctx, counter);
+        return;
+    }
     const int blocks = static_cast<int>(std::max<u64>(
         1, std::min<u64>((tiles + kRadiusWarps - 1) / kRadiusWarps, static_cast<u64>(ctx->sm_count) * 64)));
 #define LO_STRUCT_CASE(S)                                                                         \
@@ -180,6 +461,7 @@ lo_csr* radius_struct_search(lo_context* ctx, const lo_octree* t, const lo_coded
     require(r > 0.0 && std::isfinite(r), LO_INVALID_ARGUMENT,
             "kernel radius must be positive and finite");
     require(shape >= LO_SPHERE && shape <= LO_SQUARE, LO_INVALID_ARGUMENT, "unknown kernel shape");
+    ensure_float_shadows(ctx, c, t);
     ensure_ref_boxes(ctx, c, t);
     auto* out = new lo_csr;
     out->ctx = ctx;

@@ -38,6 +38,7 @@ def main():
         for method, name in ((1, "lin"), (3, "struct")):
             best = None
             for _ in range(a.reps):
+                ctx.set_timing(True)
                 csr = C.c_void_p()
                 _lib.check(L.lo_radius_range(ctx.h, tree, coded, method, 0, r, 0, n, 1, C.byref(csr)))
                 info = _lib.CsrInfo()
@@ -52,6 +53,8 @@ def main():
                     rec["members"] = info.total
                     rec["lin_bytes"] = 4 * info.total + 8 * (n + 1)
                 L.lo_csr_destroy(csr)
+                rec[f"{name}_stages"] = {k: round(v, 3) for k, v in ctx.stage_times()}
+                ctx.set_timing(False)
             rec[f"{name}_ms"] = best
         out[str(r)] = rec
         print(r, rec, flush=True)
