@@ -122,12 +122,6 @@ __global__ void radius_digest(const u64* __restrict__ offsets, const u32* __rest
     }
 }
 
-__global__ void counts_from_offsets(const u64* __restrict__ offsets, u64 m, u32* __restrict__ counts) {
-    for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < m;
-         r += (u64)gridDim.x * blockDim.x)
-        counts[r] = static_cast<u32>(offsets[r + 1] - offsets[r]);
-}
-
 struct RecArgs {  // count-pass records for the replay fill (radius_pt.cuh)
     RecPool rp;
     const u32* list = nullptr;  // fill fallback: only these tiles
