@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--radius", type=float, nargs="*", default=[3.0])
     ap.add_argument("--k", type=int, nargs="*", default=[])
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--fingerprint", action="store_true", help="also compute the FNV row digests")
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
     L = _lib.lib()
@@ -34,7 +35,8 @@ def main():
         _lib.check(L.lo_octree_build(ctx.h, coded, cfg["n_max"], C.byref(tree)))
         for r in a.radius:
             csr = C.c_void_p()
-            _lib.check(L.lo_radius_range(ctx.h, tree, coded, 1, 0, r, 0, cfg["n"], 0, C.byref(csr)))
+            _lib.check(L.lo_radius_range(ctx.h, tree, coded, 1, 0, r, 0, cfg["n"], int(a.fingerprint),
+                                         C.byref(csr)))
             L.lo_csr_destroy(csr)
         for k in a.k:
             res = C.c_void_p()
