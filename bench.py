@@ -222,9 +222,17 @@ def run_ours(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # test hooks for exercising the N > 1 code path on a single-GPU box (correctness only, the
+    # numbers of such a run mean nothing): every rank on cuda:0, collectives over gloo
+    if os.environ.get("LO_BENCH_SAME_DEVICE") == "1":
+        local = 0
+    backend = os.environ.get("LO_BENCH_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     L = _lib.lib()
     ctx = lo.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
