@@ -404,6 +404,8 @@ def run_ours(args, cfg):
                     _lib.check(L.lo_csr_download_async(ctx.h, csr, hc[i], hf[i], None, None))
                     L.lo_csr_destroy(csr)
                 free(coded, tree)
+                # each step ends with its counts + digests on the host (letting them trail into the
+                # next step measured slower: the deferred result buffers grow the memory pool)
                 _lib.check(L.lo_context_synchronize(ctx.h))
 
         e2e_run(max(2, args.warmup // 2))
