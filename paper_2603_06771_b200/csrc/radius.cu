@@ -183,8 +183,6 @@ static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
     LO_CHECK_LAUNCH();
 }
 
-// Max records per tile for the fused count -> replay fill (128 buffers x 256 B = 32 KB).
-constexpr u32 kRecCap = 128;
 
 static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded* c, int shape,
                              double r, const Queries& q, bool fingerprint) {
@@ -209,31 +207,10 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
         static const bool no_fuse = std::getenv("LO_RADIUS_NO_FUSE") != nullptr;
         if (q.m && !no_fuse && float_path(t, c, q, r)) {
             try {
-                // one persistent block: rec_off[tiles] u64 | alloc u64 | rec_n[tiles] |
-                // overflow list[tiles] | ovf_n | pool (records of 256 B).  The pool is sized for
-                // the worst case (kRecCap per tile) within a quarter of the free memory; tiles that
-                // find it exhausted fall back to the fill walk.
-                const u64 head = 8 * (tiles + 1) + 4 * (2 * tiles + 1);
-                u64 recs = tiles * kRecCap;
-                if (head + 16 + recs * 256 > ctx->arena_bytes) {  // growing: respect free memory
-                    size_t free_b = 0, total_b = 0;
-                    LO_CUDA(cudaMemGetInfo(&free_b, &total_b));
-                    const u64 budget = (free_b + ctx->arena_bytes) / 4;
-                    recs = std::min<u64>(recs, budget > head ? (budget - head) / 256 : 0);
-                } else {  // reuse whatever the arena holds
-                    recs = (ctx->arena_bytes - head - 16) / 256;
-                }
-                recs = std::max<u64>(recs, kRecChunk * 2);
-                unsigned char* base = static_cast<unsigned char*>(arena(ctx, head + 16 + recs * 256));
-                ra.rp.rec_off = reinterpret_cast<u64*>(base);
-                ra.rp.alloc = ra.rp.rec_off + tiles;
-                ra.rp.rec_n = reinterpret_cast<u32*>(ra.rp.alloc + 1);
-                ovf = ra.rp.rec_n + tiles;
-                ovf_n = ovf + tiles;
-                ra.rp.pool = reinterpret_cast<u32*>(base + ((head + 15) / 16) * 16);
-                ra.rp.pool_recs = recs;
-                ra.rp.cap = kRecCap;
-                LO_CUDA(cudaMemsetAsync(ra.rp.alloc, 0, 8, ctx->stream));
+                RecSetup rs = setup_records(ctx, tiles, kRecCap);
+                ra.rp = rs.rp;
+                ovf = rs.ovf;
+                ovf_n = rs.ovf_n;
             } catch (const Error&) {  // not enough memory for the records: two-walk path
                 ra = RecArgs{};
                 ovf = ovf_n = nullptr;
@@ -249,33 +226,8 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
         out->indices = dalloc_t<u32>(ctx, out->total);
         stage_begin(ctx, "radius_fill");
         if (q.m && ra.rp.pool) {
-            LO_CUDA(cudaMemsetAsync(ovf_n, 0, 4, ctx->stream));
-            const int rb = static_cast<int>(std::max<u64>(
-                1, std::min<u64>((tiles + kReplayWarps - 1) / kReplayWarps, ctx->sm_count * 16ull)));
-            // short rows: buffer-major stores stay line-local; long rows: row-major so every
-            // output line completes while hot (measured crossover ~ 64 members per row)
-            static const u64 row_major_min = [] {  // mean row length from which rows go row-major
-                const char* e = std::getenv("LO_REPLAY_ROW_MAJOR_MIN");
-                return e ? std::strtoull(e, nullptr, 10) : 96ull;
-            }();
-            if (out->total < row_major_min * q.m)
-                radius_replay_bm_kernel<<<rb, 128, 0, ctx->stream>>>(ra.rp, q.m, out->offsets, out->indices,
-                                                                    ovf, ovf_n);
-            else {
-                static const bool attr = [] {
-                    LO_CUDA(cudaFuncSetAttribute(radius_replay_kernel,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(kReplaySmem)));
-                    return true;
-                }();
-                (void)attr;
-                const int rr = static_cast<int>(std::max<u64>(
-                    1, std::min<u64>((tiles + kReplayWarps - 1) / kReplayWarps, ctx->sm_count * 6ull)));
-                radius_replay_kernel<<<rr, 32 * kReplayWarps, kReplaySmem, ctx->stream>>>(
-                    ra.rp, q.m, out->offsets, out->indices, ovf, ovf_n);
-            }
-            LO_CHECK_LAUNCH();
-            const u32 n_ovf = read_scalar(ctx, ovf_n);
+            const u32 n_ovf = replay_records(ctx, RecSetup{ra.rp, ovf, ovf_n}, q.m, out->offsets,
+                                             out->indices, out->total);
             static const bool debug = std::getenv("LO_DEBUG") != nullptr;
             if (debug)
                 std::fprintf(stderr, "[lo] radius r=%g: %u of %llu tiles overflowed the %u-buffer records\n",

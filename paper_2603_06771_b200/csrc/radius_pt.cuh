@@ -13,6 +13,9 @@
 // Uncertainty-band points (search_common.cuh) are decided by the exact FP64 predicate.
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "radius_float.cuh"
 
 namespace lo {
@@ -324,6 +327,76 @@ static __global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_ker
             cursor += adv;
         }
     }
+}
+
+// Max records per tile for the fused count -> replay fill (128 buffers x 256 B = 32 KB).
+constexpr u32 kRecCap = 128;
+
+// The count pass's record pool in the persistent context arena: rec_off[tiles] u64 | alloc u64 |
+// rec_n[tiles] | overflow list[tiles] | ovf_n | pool (records of 256 B).  The pool is sized for
+// the worst case (cap per tile) within a quarter of the free memory; tiles that find it
+// exhausted fall back to the fill walk.  Throws LO_OUT_OF_MEMORY when even that cannot be had.
+struct RecSetup {
+    RecPool rp;
+    u32* ovf = nullptr;
+    u32* ovf_n = nullptr;
+};
+static inline RecSetup setup_records(lo_context* ctx, u64 tiles, u32 cap) {
+    RecSetup rs;
+    const u64 head = 8 * (tiles + 1) + 4 * (2 * tiles + 1);
+    u64 recs = tiles * cap;
+    if (head + 16 + recs * 256 > ctx->arena_bytes) {  // growing: respect free memory
+        size_t free_b = 0, total_b = 0;
+        LO_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const u64 budget = (free_b + ctx->arena_bytes) / 4;
+        recs = std::min<u64>(recs, budget > head ? (budget - head) / 256 : 0);
+    } else {  // reuse whatever the arena holds
+        recs = (ctx->arena_bytes - head - 16) / 256;
+    }
+    recs = std::max<u64>(recs, kRecChunk * 2);
+    unsigned char* base = static_cast<unsigned char*>(arena(ctx, head + 16 + recs * 256));
+    rs.rp.rec_off = reinterpret_cast<u64*>(base);
+    rs.rp.alloc = rs.rp.rec_off + tiles;
+    rs.rp.rec_n = reinterpret_cast<u32*>(rs.rp.alloc + 1);
+    rs.ovf = rs.rp.rec_n + tiles;
+    rs.ovf_n = rs.ovf + tiles;
+    rs.rp.pool = reinterpret_cast<u32*>(base + ((head + 15) / 16) * 16);
+    rs.rp.pool_recs = recs;
+    rs.rp.cap = cap;
+    LO_CUDA(cudaMemsetAsync(rs.rp.alloc, 0, 8, ctx->stream));
+    return rs;
+}
+
+// Fill by replaying the records into the CSR (offsets[m+1], out); returns how many tiles
+// overflowed (their ids in rs.ovf) and need the fill walk.
+static inline u32 replay_records(lo_context* ctx, const RecSetup& rs, u64 m, const u64* offsets, u32* out,
+                                 u64 total) {
+    const u64 tiles = (m + 31) / 32;
+    LO_CUDA(cudaMemsetAsync(rs.ovf_n, 0, 4, ctx->stream));
+    // short rows: buffer-major stores stay line-local; long rows: row-major so every output line
+    // completes while hot (measured crossover ~ 64-96 members per row on cfg0 / cfg1 / cfg4)
+    static const u64 row_major_min = [] {
+        const char* e = std::getenv("LO_REPLAY_ROW_MAJOR_MIN");
+        return e ? std::strtoull(e, nullptr, 10) : 96ull;
+    }();
+    if (total < row_major_min * m) {
+        const int rb = static_cast<int>(std::max<u64>(
+            1, std::min<u64>((tiles + kReplayWarps - 1) / kReplayWarps, ctx->sm_count * 16ull)));
+        radius_replay_bm_kernel<<<rb, 128, 0, ctx->stream>>>(rs.rp, m, offsets, out, rs.ovf, rs.ovf_n);
+    } else {
+        static const bool attr = [] {
+            LO_CUDA(cudaFuncSetAttribute(radius_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kReplaySmem)));
+            return true;
+        }();
+        (void)attr;
+        const int rr = static_cast<int>(std::max<u64>(
+            1, std::min<u64>((tiles + kReplayWarps - 1) / kReplayWarps, ctx->sm_count * 6ull)));
+        radius_replay_kernel<<<rr, 32 * kReplayWarps, kReplaySmem, ctx->stream>>>(rs.rp, m, offsets, out, rs.ovf,
+                                                                                rs.ovf_n);
+    }
+    LO_CHECK_LAUNCH();
+    return read_scalar(ctx, rs.ovf_n);
 }
 
 template <int SHAPE, bool FILL>

@@ -28,6 +28,21 @@ namespace lo {
 // the 32-slot buffers; each slot carries the mask of queries that reached its leaf as Intersects,
 // so a query that contains (or skipped) that leaf never counts its points as singles.
 enum { kRelU = 3 };  // "uncertain": decide in FP64
+constexpr u32 kStructRangeCap = 16;  // count-pass range slots per query (more: the tile is re-walked)
+
+// Ranges of the count pass (per query scratch) into the ranges CSR; overflowed tiles are written
+// by the fill walk instead.
+__global__ void struct_copy_ranges(const u32* __restrict__ rscratch, const u32* __restrict__ nrng, u64 m,
+                                   const u64* __restrict__ r_off, const u32* __restrict__ rec_n,
+                                   u32* __restrict__ ranges) {
+    for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < m * kStructRangeCap;
+         e += (u64)gridDim.x * blockDim.x) {
+        const u64 qi = e / kStructRangeCap, j = e - qi * kStructRangeCap;
+        if (j >= nrng[qi] || rec_n[qi / 32] == kRecOverflow) continue;
+        const uint2 v = reinterpret_cast<const uint2*>(rscratch)[e];
+        reinterpret_cast<uint2*>(ranges)[r_off[qi] + j] = v;
+    }
+}
 
 template <int SHAPE>
 __device__ __forceinline__ int classify_ref_f(const float4& q, const float4& lo, const float4& hi,
@@ -71,32 +86,86 @@ struct StructShared {
 };
 
 // Tests the buffer (lane j = slot j) against every query whose bit is in qmask; a query counts a
-// slot only if the slot's want mask holds it.  Count pass: lane L adds its members to `ns`;
-// fill pass: members of query L go to srow_base + cursor (coalesced per query).
-template <int SHAPE, bool FILL>
+// slot only if the slot's want mask holds it.  Count pass (records): query L's membership mask of
+// the buffer lands in S.msk[L] (quads of queries per ballot round for the packed shapes).  Fill
+// walk: members of query L go to singles[srow_L + cursor] (coalesced per query).
+template <int SHAPE, int MODE>
 __device__ __forceinline__ void struct_buffer(StructShared& SS, u32 qmask, int lane, float lo_thr,
                                               float hi_thr, const double* __restrict__ px,
                                               const double* __restrict__ py, const double* __restrict__ pz,
                                               double r, double r2, u32* __restrict__ singles, u64 srow,
                                               u32& ns) {
+    constexpr bool FILL = MODE != 0;
+    constexpr bool kPacked = SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE;
     PtShared& S = SS.pt;
     const float4 P = S.buf[lane];
     const u32 idx = __float_as_uint(P.w);
     const u32 sw = SS.sw[lane];
     const u32 lt = (1u << lane) - 1u;
+    const u32 lo_bits = __float_as_uint(lo_thr);
+    const u32 band_bits = __float_as_uint(hi_thr) - lo_bits;
+    const u64 PX = pack2(P.x, P.x), PY = pack2(P.y, P.y), PZ = pack2(P.z, P.z);
+    if (!FILL && kPacked) {
+        u32 qm = (qmask | (qmask >> 1) | (qmask >> 2) | (qmask >> 3)) & 0x11111111u;
+        S.msk[lane] = 0u;
+        __syncwarp();
+        while (qm) {
+            const int b = __ffs(qm) - 1;
+            qm &= qm - 1;
+            const float4 X = *reinterpret_cast<const float4*>(&S.qx[b]);
+            const float4 Y = *reinterpret_cast<const float4*>(&S.qy[b]);
+            const u64 dxa = fsub2(PX, pack2(X.x, X.y)), dxb = fsub2(PX, pack2(X.z, X.w));
+            const u64 dya = fsub2(PY, pack2(Y.x, Y.y)), dyb = fsub2(PY, pack2(Y.z, Y.w));
+            u64 da = fmul2(dxa, dxa), db = fmul2(dxb, dxb);
+            da = ffma2(dya, dya, da);
+            db = ffma2(dyb, dyb, db);
+            if (SHAPE == LO_SPHERE) {
+                const float4 Z = *reinterpret_cast<const float4*>(&S.qz[b]);
+                const u64 dza = fsub2(PZ, pack2(Z.x, Z.y)), dzb = fsub2(PZ, pack2(Z.z, Z.w));
+                da = ffma2(dza, dza, da);
+                db = ffma2(dzb, dzb, db);
+            }
+            float v[4];
+            unpack2(da, v[0], v[1]);
+            unpack2(db, v[2], v[3]);
+            bool wq[4];
+            u32 in[4];
+            u32 wband = ~0u;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                wq[t] = (sw >> (b + t)) & 1u;
+                in[t] = __ballot_sync(~0u, wq[t] && v[t] < lo_thr);
+                if (wq[t]) wband = min(wband, __float_as_uint(v[t]) - lo_bits);
+            }
+            if (__any_sync(~0u, wband < band_bits)) {  // rare: band points, FP64 decides
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const u32 h = __ballot_sync(~0u, wq[t] && v[t] < hi_thr);
+                    if (h ^ in[t]) in[t] = band_fix<SHAPE>(in[t], h ^ in[t], S, b + t, lane, idx, px, py, pz, r, r2);
+                }
+            }
+            if (lane == 0) *reinterpret_cast<uint4*>(&S.msk[b]) = make_uint4(in[0], in[1], in[2], in[3]);
+        }
+        __syncwarp();
+        ns += __popc(S.msk[lane]);
+        return;
+    }
+    if (!FILL) {
+        S.msk[lane] = 0u;
+        __syncwarp();
+    }
     u32 pm = (qmask | (qmask >> 1)) & 0x55555555u;
     while (pm) {
         const int b = __ffs(pm) - 1;
         pm &= pm - 1;
         float v0, v1;
-        if (SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE) {
-            const u64 PX = pack2(P.x, P.x), PY = pack2(P.y, P.y);
+        if (kPacked) {
             const u64 dx = fsub2(PX, *reinterpret_cast<const u64*>(&S.qx[b]));
             const u64 dy = fsub2(PY, *reinterpret_cast<const u64*>(&S.qy[b]));
             u64 d2 = fmul2(dx, dx);
             d2 = ffma2(dy, dy, d2);
             if (SHAPE == LO_SPHERE) {
-                const u64 dz = fsub2(pack2(P.z, P.z), *reinterpret_cast<const u64*>(&S.qz[b]));
+                const u64 dz = fsub2(PZ, *reinterpret_cast<const u64*>(&S.qz[b]));
                 d2 = ffma2(dz, dz, d2);
             }
             unpack2(d2, v0, v1);
@@ -118,33 +187,55 @@ __device__ __forceinline__ void struct_buffer(StructShared& SS, u32 qmask, int l
             const u64 s1 = __shfl_sync(~0u, srow, b + 1);
             if ((in0 >> lane) & 1u) singles[s0 + c0 + __popc(in0 & lt)] = idx;
             if ((in1 >> lane) & 1u) singles[s1 + c1 + __popc(in1 & lt)] = idx;
+            ns += lane == b ? __popc(in0) : (lane == b + 1 ? __popc(in1) : 0u);
+        } else if (lane == 0) {
+            *reinterpret_cast<uint2*>(&S.msk[b]) = make_uint2(in0, in1);
         }
-        ns += lane == b ? __popc(in0) : (lane == b + 1 ? __popc(in1) : 0u);
+    }
+    if (!FILL) {
+        __syncwarp();
+        ns += __popc(S.msk[lane]);
     }
 }
 
-template <int SHAPE, bool FILL>
+// MODE 0: count walk (counts, range / single counts, ranges into per-query scratch slots,
+//         per-buffer records for the singles replay);
+// MODE 2: full fill walk (ranges + singles) over `tile_list` (overflowed tiles) or every tile.
+template <int SHAPE, int MODE>
 __global__ void __launch_bounds__(kPtThreads, 8) struct_pt_kernel(
     const TNodeF* __restrict__ tf, const float4* __restrict__ rbf, const double* __restrict__ rb,
     const float4* __restrict__ pf, const double* __restrict__ px, const double* __restrict__ py,
     const double* __restrict__ pz, Queries q, FloatTest ft, float compact, double r, double r2,
     u32* __restrict__ counts, u32* __restrict__ nrng, u32* __restrict__ nsgl,
     const u64* __restrict__ r_off, u32* __restrict__ ranges, const u64* __restrict__ s_off,
-    u32* __restrict__ singles, u64* tile_counter) {
+    u32* __restrict__ singles, u64* tile_counter, RecPool rp, const u32* __restrict__ tile_list,
+    u64 list_n, u32* __restrict__ rscratch) {
+    constexpr bool FILL = MODE != 0;
     __shared__ StructShared shared_s[kPtWarps];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     StructShared& SS = shared_s[w];
     PtShared& S = SS.pt;
-    const u64 ntiles = (q.m + 31) / 32;
+    const u64 ntiles = tile_list ? list_n : (q.m + 31) / 32;
     const int cl = lane & 7, grp = lane >> 3;
     constexpr bool kSq = SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE;
     const float lo_thr = kSq ? ft.t_lo : ft.r_lo;
     const float hi_thr = kSq ? ft.t_hi : ft.r_hi;
+    u64 chunk_base = 0;  // count pass: this warp's current record chunk (in records)
+    u32 chunk_left = 0;
     for (;;) {
         u64 tile = 0;
         if (lane == 0) tile = atomicAdd(reinterpret_cast<unsigned long long*>(tile_counter), 1ull);
         tile = __shfl_sync(~0u, tile, 0);
         if (tile >= ntiles) break;
+        if (tile_list) tile = tile_list[tile];
+        if (MODE == 0 && rp.pool && chunk_left < rp.cap) {
+            u64 base = 0;
+            if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long*>(rp.alloc),
+                                            static_cast<unsigned long long>(kRecChunk));
+            base = __shfl_sync(~0u, base, 0);
+            chunk_base = base;
+            chunk_left = base + kRecChunk <= rp.pool_recs ? kRecChunk : 0u;
+        }
         const u64 qi = tile * 32 + lane;
         const bool active = qi < q.m;
         double cx = 0.0, cy = 0.0, cz = 0.0;
@@ -178,9 +269,18 @@ __global__ void __launch_bounds__(kPtThreads, 8) struct_pt_kernel(
             }
         }
         const bool gcompact = fmaxf(fmaxf(gh[0] - gl[0], gh[1] - gl[1]), gh[2] - gl[2]) <= compact;
-        u32 fill = 0, qmask = 0;
+        u32 fill = 0, qmask = 0, nrec = 0;
+        u32* rec_tile = (MODE == 0 && rp.pool && chunk_left >= rp.cap) ? rp.pool + chunk_base * 64 : nullptr;
         auto flush = [&]() {
-            struct_buffer<SHAPE, FILL>(SS, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2, singles, srow, ns);
+            struct_buffer<SHAPE, MODE>(SS, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2, singles, srow, ns);
+            if (MODE == 0 && rec_tile) {
+                if (nrec < rp.cap) {
+                    u32* R = rec_tile + nrec * 64;
+                    R[lane] = __float_as_uint(S.buf[lane].w);
+                    R[32 + lane] = S.msk[lane];
+                }
+                ++nrec;
+            }
         };
         int sp = 1;
         if (lane == 0) S.stack[0] = 0;
@@ -203,10 +303,14 @@ __global__ void __launch_bounds__(kPtThreads, 8) struct_pt_kernel(
                     rel = relation<SHAPE>(cx, cy, cz, r, r2, box);
                 }
                 if (rel == kContains) {
+                    // count pass: ranges go to this query's scratch slots (copied after the scan)
+                    u32* rs_q = MODE == 0 && rscratch ? rscratch + 2 * static_cast<u64>(qi) * kStructRangeCap : nullptr;
                     if (nr > 0 && last_e == nd.begin) {
                         if (FILL) rrow[2 * (nr - 1) + 1] = nd.end;
+                        else if (rs_q && nr <= kStructRangeCap) rs_q[2 * (nr - 1) + 1] = nd.end;
                     } else {
                         if (FILL) rrow[2 * nr] = nd.begin, rrow[2 * nr + 1] = nd.end;
+                        else if (rs_q && nr < kStructRangeCap) rs_q[2 * nr] = nd.begin, rs_q[2 * nr + 1] = nd.end;
                         ++nr;
                     }
                     last_e = nd.end;
@@ -267,10 +371,23 @@ __global__ void __launch_bounds__(kPtThreads, 8) struct_pt_kernel(
             __syncwarp();
             flush();
         }
-        if (!FILL && active) {
+        if (MODE == 0 && active) {
             counts[qi] = count + ns;
             nrng[qi] = nr;
             nsgl[qi] = ns;
+        }
+        if (MODE == 0 && rp.pool) {
+            // a query with more ranges than its scratch slots sends the tile to the fill walk
+            const bool rovf = __any_sync(~0u, rscratch && nr > kStructRangeCap);
+            const bool ok = rec_tile && nrec <= rp.cap && !rovf;
+            if (lane == 0) {
+                rp.rec_n[tile] = ok ? nrec : kRecOverflow;
+                rp.rec_off[tile] = chunk_base;
+            }
+            if (ok) {
+                chunk_base += nrec;
+                chunk_left -= nrec;
+            }
         }
         __syncwarp();
     }
@@ -406,36 +523,48 @@ static int grid_rows(lo_context* ctx, u64 m) {
     return static_cast<int>(std::max<u64>(1, std::min<u64>((m + 255) / 256, ctx->sm_count * 16ull)));
 }
 
+static bool struct_float_path(const lo_octree* t, const lo_coded* c, const Queries& q, double r) {
+    return make_float_test(r, std::max(c->bmax, q.bmax)).enabled && q.f && t->tf && c->pf && t->rbf;
+}
+
+// MODE 0 count (+ records, range slots), 2 full fill walk (over `list` when given).
+template <int MODE>
+static void launch_struct_pt(lo_context* ctx, int shape, const lo_octree* t, const lo_coded* c, const Queries& q,
+                             double r, lo_csr* out, u32* nrng, u32* nsgl, RecPool rp = RecPool{},
+                             const u32* list = nullptr, u64 list_n = 0, u32* rscratch = nullptr) {
+    const double r2 = r * r;  // SearchKernel ctor (geometry.hpp:107)
+    const u64 tiles = list ? list_n : (q.m + 31) / 32;
+    const FloatTest ft = make_float_test(r, std::max(c->bmax, q.bmax));
+    u64* counter = dalloc_t<u64>(ctx, 1);
+    LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
+    const int pblocks = static_cast<int>(std::max<u64>(
+        1, std::min<u64>((tiles + kPtWarps - 1) / kPtWarps, static_cast<u64>(ctx->sm_count) * 8)));
+    const float compact = static_cast<float>(4.0 * r);
+#define LO_STRUCT_PT(S)                                                                                 \
+    case S:                                                                                             \
+        struct_pt_kernel<S, MODE><<<pblocks, kPtThreads, 0, ctx->stream>>>(                             \
+            t->tf, t->rbf, t->rb, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, out->counts, nrng,     \
+            nsgl, out->range_offsets, out->ranges, out->single_offsets, out->singles, counter, rp, list, \
+            list_n, rscratch);                                                                          \
+        break;
+    switch (shape) {
+        LO_STRUCT_PT(LO_SPHERE)
+        LO_STRUCT_PT(LO_CIRCLE)
+        LO_STRUCT_PT(LO_CUBE)
+        LO_STRUCT_PT(LO_SQUARE)
+        default: throw Error(LO_INVALID_ARGUMENT, "unknown kernel shape");
+    }
+#undef LO_STRUCT_PT
+    LO_CHECK_LAUNCH();
+    dfree(ctx, counter);
+}
+
+// The exact FP64 fallback (the FP32 filter disabled for this radius / cloud extent).
 template <bool FILL>
 static void launch_struct(lo_context* ctx, int shape, const lo_octree* t, const lo_coded* c,
                           const Queries& q, double r, lo_csr* out, u32* nrng, u32* nsgl) {
     const double r2 = r * r;  // SearchKernel ctor (geometry.hpp:107)
     const u64 tiles = (q.m + 31) / 32;
-    const FloatTest ft = make_float_test(r, std::max(c->bmax, q.bmax));
-    if (ft.enabled && q.f && t->tf && c->pf && t->rbf) {
-        u64* counter = dalloc_t<u64>(ctx, 1);
-        LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
-        const int pblocks = static_cast<int>(std::max<u64>(
-            1, std::min<u64>((tiles + kPtWarps - 1) / kPtWarps, static_cast<u64>(ctx->sm_count) * 8)));
-        const float compact = static_cast<float>(4.0 * r);
-#define LO_STRUCT_PT(S)                                                                              \
-    case S:                                                                                          \
-        struct_pt_kernel<S, FILL><<<pblocks, kPtThreads, 0, ctx->stream>>>(                          \
-            t->tf, t->rbf, t->rb, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, out->counts, nrng,  \
-            nsgl, out->range_offsets, out->ranges, out->single_offsets, out->singles, counter);      \
-        break;
-        switch (shape) {
-            LO_STRUCT_PT(LO_SPHERE)
-            LO_STRUCT_PT(LO_CIRCLE)
-            LO_STRUCT_PT(LO_CUBE)
-            LO_STRUCT_PT(LO_SQUARE)
-            default: throw Error(LO_INVALID_ARGUMENT, "unknown kernel shape");
-        }
-#undef LO_STRUCT_PT
-        LO_CHECK_LAUNCH();
-        dfree(ctx, counter);
-        return;
-    }
     const int blocks = static_cast<int>(std::max<u64>(
         1, std::min<u64>((tiles + kRadiusWarps - 1) / kRadiusWarps, static_cast<u64>(ctx->sm_count) * 64)));
 #define LO_STRUCT_CASE(S)                                                                         \
@@ -467,7 +596,7 @@ lo_csr* radius_struct_search(lo_context* ctx, const lo_octree* t, const lo_coded
     out->ctx = ctx;
     out->rows = q.m;
     out->is_struct = true;
-    u32 *nrng = nullptr, *nsgl = nullptr;
+    u32 *nrng = nullptr, *nsgl = nullptr, *rscratch = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     try {
         LO_CUDA(cudaEventCreate(&e0));
@@ -479,8 +608,23 @@ lo_csr* radius_struct_search(lo_context* ctx, const lo_octree* t, const lo_coded
         out->single_offsets = dalloc_t<u64>(ctx, q.m + 1);
         nrng = dalloc_t<u32>(ctx, q.m);
         nsgl = dalloc_t<u32>(ctx, q.m);
+        const bool fast = q.m && struct_float_path(t, c, q, r);
+        RecSetup rs;
+        if (fast) {
+            try {
+                rs = setup_records(ctx, (q.m + 31) / 32, kRecCap);
+                rscratch = dalloc_t<u32>(ctx, 2 * q.m * kStructRangeCap);
+            } catch (const Error&) {  // no room for records / range slots: fill walks instead
+                rs = RecSetup{};
+                dfree(ctx, rscratch);
+                rscratch = nullptr;
+            }
+        }
         stage_begin(ctx, "struct_count");
-        if (q.m) launch_struct<false>(ctx, shape, t, c, q, r, out, nrng, nsgl);
+        if (fast)
+            launch_struct_pt<0>(ctx, shape, t, c, q, r, out, nrng, nsgl, rs.rp, nullptr, 0, rscratch);
+        else if (q.m)
+            launch_struct<false>(ctx, shape, t, c, q, r, out, nrng, nsgl);
         stage_end(ctx);
         exclusive_scan_u32_to_u64(ctx, out->counts, out->offsets, q.m);
         exclusive_scan_u32_to_u64(ctx, nrng, out->range_offsets, q.m);
@@ -491,7 +635,21 @@ lo_csr* radius_struct_search(lo_context* ctx, const lo_octree* t, const lo_coded
         out->ranges = dalloc_t<u32>(ctx, 2 * out->total_ranges);
         out->singles = dalloc_t<u32>(ctx, out->total_singles);
         stage_begin(ctx, "struct_fill");
-        if (q.m) launch_struct<true>(ctx, shape, t, c, q, r, out, nrng, nsgl);
+        if (fast && rs.rp.pool) {
+            // singles: replay of the count pass's records (want-masked memberships); ranges: a
+            // walk without leaf points; overflowed tiles: the full fill walk
+            const u32 n_ovf = replay_records(ctx, rs, q.m, out->single_offsets, out->singles, out->total_singles);
+            if (out->total_ranges) {
+                struct_copy_ranges<<<grid_rows(ctx, q.m * kStructRangeCap), 256, 0, ctx->stream>>>(
+                    rscratch, nrng, q.m, out->range_offsets, rs.rp.rec_n, out->ranges);
+                LO_CHECK_LAUNCH();
+            }
+            if (n_ovf) launch_struct_pt<2>(ctx, shape, t, c, q, r, out, nrng, nsgl, RecPool{}, rs.ovf, n_ovf);
+        } else if (fast) {
+            launch_struct_pt<2>(ctx, shape, t, c, q, r, out, nrng, nsgl);
+        } else if (q.m) {
+            launch_struct<true>(ctx, shape, t, c, q, r, out, nrng, nsgl);
+        }
         stage_end(ctx);
         if (fingerprint) {
             out->fps = dalloc_t<u64>(ctx, q.m);
@@ -508,6 +666,7 @@ lo_csr* radius_struct_search(lo_context* ctx, const lo_octree* t, const lo_coded
     } catch (...) {
         dfree(ctx, nrng);
         dfree(ctx, nsgl);
+        dfree(ctx, rscratch);
         free_csr_buffers(ctx, out);
         delete out;
         if (e0) cudaEventDestroy(e0);
@@ -516,6 +675,7 @@ lo_csr* radius_struct_search(lo_context* ctx, const lo_octree* t, const lo_coded
     }
     dfree(ctx, nrng);
     dfree(ctx, nsgl);
+    dfree(ctx, rscratch);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return out;
