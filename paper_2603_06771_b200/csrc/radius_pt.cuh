@@ -204,19 +204,24 @@ static __global__ void __launch_bounds__(128) radius_replay_bm_kernel(
         const u64 tbase = offsets[tile * 32];
         u32* out_tile = out + tbase;
         u32 cursor = qi < m ? static_cast<u32>(offsets[qi] - tbase) : 0u;
+        asm("" : "+l"(out_tile));  // keep the stores as 32-bit offsets from one base
         const u32* R = rp.pool + rp.rec_off[tile] * 64;
-        for (u32 b = 0; b < n; ++b, R += 64) {
-            const u32 idx = __ldg(R + lane);
-            const u32 mk = __ldg(R + 32 + lane);
+        // record b + 1 is loaded while record b is written (the loads were exposed before)
+        u32 idx = 0, mk = 0;
+        if (n) idx = __ldg(R + lane), mk = __ldg(R + 32 + lane);
+        for (u32 b = 0; b < n; ++b) {
+            u32 idx_n = 0, mk_n = 0;
+            if (b + 1 < n) idx_n = __ldg(R + 64 * (b + 1) + lane), mk_n = __ldg(R + 64 * (b + 1) + 32 + lane);
             unsigned nz = __ballot_sync(~0u, mk != 0);
             while (nz) {
                 const int L = __ffs(nz) - 1;
                 nz &= nz - 1;
                 const u32 mL = __shfl_sync(~0u, mk, L);
                 const u32 cL = __shfl_sync(~0u, cursor, L);
-                if ((mL >> lane) & 1u) out_tile[cL + __popc(mL & lt)] = idx;
+                if ((mL >> lane) & 1u) __stcg(out_tile + (cL + __popc(mL & lt)), idx);
             }
             cursor += __popc(mk);
+            idx = idx_n, mk = mk_n;
         }
     }
 }
