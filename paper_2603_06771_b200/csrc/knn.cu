@@ -30,6 +30,10 @@ struct LaneHeap {
     u32* hi;
     u32 size;
 
+    __device__ __forceinline__ bool after(double a, u32 ia, double b, u32 ib) const {
+        return lo::after(a, ia, b, ib);
+    }
+
     __device__ __forceinline__ void push(double d, u32 i) {
         u32 pos = size++;
         while (pos > 0) {
@@ -329,20 +333,30 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
     LO_CUDA(cudaEventCreate(&e0));
     LO_CUDA(cudaEventCreate(&e1));
     double* gd = nullptr;
+    float* gk = nullptr;
     u32* gi = nullptr;
     try {
         LO_CUDA(cudaEventRecord(e0, ctx->stream));
         out->idx = dalloc_t<u32>(ctx, q.m * kh);
         out->dist = dalloc_t<double>(ctx, q.m * kh);
         const bool use_float = q.f && t->tf && c->pf;
-        const size_t per_warp_heap = static_cast<size_t>(kh) * 32 * 12;
+        // FP32-filtered kernel: (key f32, index) heap entries; exact fallback: (f64, index)
+        const bool keyed = use_float && kh >= 32;  // compact heap entries where occupancy binds
+        const size_t per_warp_heap = static_cast<size_t>(kh) * 32 * (keyed ? 8 : 12);
         const size_t per_warp_fixed =
             use_float ? kKnnFixed : sizeof(u32) * kStackCap + 96 * sizeof(double);
         const bool global_heap = per_warp_heap + per_warp_fixed > static_cast<size_t>(kKnnSmemBudget);
+        // warps per block: the most resident warps per SM under the shared-memory budget
         int warps = 4;
-        if (!global_heap)
-            while (warps > 1 && warps * (per_warp_heap + per_warp_fixed) > static_cast<size_t>(kKnnSmemBudget))
-                warps >>= 1;
+        if (!global_heap) {
+            int best = 0;
+            for (int w = 4; w >= 1; w >>= 1) {
+                const size_t blk = w * (per_warp_heap + per_warp_fixed);
+                if (blk > static_cast<size_t>(kKnnSmemBudget)) continue;
+                const int resident = w * std::min(16, static_cast<int>(220 * 1024 / blk));
+                if (resident > best) best = resident, warps = w;
+            }
+        }
         const size_t smem = warps * (per_warp_fixed + (global_heap ? 0 : per_warp_heap));
         const u64 tiles = (q.m + 31) / 32;
         int per_sm = std::max(1, static_cast<int>(220 * 1024 / std::max<size_t>(smem, 1)));
@@ -357,29 +371,32 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
             u64* counter = dalloc_t<u64>(ctx, 1);
             LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
             if (global_heap) {
-                gd = dalloc_t<double>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
+                gk = dalloc_t<float>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
                 gi = dalloc_t<u32>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
-                LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<true, 0>,
+                LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<true, 0, true>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                knn_float_kernel<true, 0><<<blocks, 32 * warps, smem, ctx->stream>>>(
+                knn_float_kernel<true, 0, true><<<blocks, 32 * warps, smem, ctx->stream>>>(
                     t->tf, c->pf, c->x, c->y, c->z, c->n, q, seed_base, seed_half, E, kh, out->idx,
-                    out->dist, gd, gi, counter);
+                    out->dist, gk, gi, counter);
             } else {
                 // common k compile to fixed-depth, unrolled heap sifts
-#define LO_KNN_LAUNCH(KC)                                                                                 \
+#define LO_KNN_LAUNCH(KC, KEYED)                                                                          \
     do {                                                                                                  \
-        LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<false, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     static_cast<int>(smem)));                                            \
-        knn_float_kernel<false, KC><<<blocks, 32 * warps, smem, ctx->stream>>>(                           \
+        LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<false, KC, KEYED>,                                  \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));\
+        knn_float_kernel<false, KC, KEYED><<<blocks, 32 * warps, smem, ctx->stream>>>(                    \
             t->tf, c->pf, c->x, c->y, c->z, c->n, q, seed_base, seed_half, E, kh, out->idx, out->dist,    \
             nullptr, nullptr, counter);                                                                   \
     } while (0)
                 switch (kh) {
-                    case 8: LO_KNN_LAUNCH(8); break;
-                    case 16: LO_KNN_LAUNCH(16); break;
-                    case 32: LO_KNN_LAUNCH(32); break;
-                    case 64: LO_KNN_LAUNCH(64); break;
-                    default: LO_KNN_LAUNCH(0); break;
+                    case 8: LO_KNN_LAUNCH(8, false); break;
+                    case 16: LO_KNN_LAUNCH(16, false); break;
+                    case 32: LO_KNN_LAUNCH(32, true); break;
+                    case 64: LO_KNN_LAUNCH(64, true); break;
+                    default:
+                        if (keyed) LO_KNN_LAUNCH(0, true);
+                        else LO_KNN_LAUNCH(0, false);
+                        break;
                 }
 #undef LO_KNN_LAUNCH
             }
@@ -418,6 +435,7 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
         dfree(ctx, out->dist);
         dfree(ctx, out->fps);
         dfree(ctx, gd);
+        dfree(ctx, gk);
         dfree(ctx, gi);
         delete out;
         cudaEventDestroy(e0);
@@ -425,6 +443,7 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
         throw;
     }
     dfree(ctx, gd);
+    dfree(ctx, gk);
     dfree(ctx, gi);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

@@ -14,6 +14,8 @@
 // it, and candidates already seen in the window are skipped by index.
 #pragma once
 
+#include <type_traits>
+
 #include "radius_float.cuh"
 
 namespace lo {
@@ -53,36 +55,139 @@ __device__ __forceinline__ float knn_threshold(double w, float E) {
     return __fmaf_ru(3.0f, M, wf);
 }
 
+// The per-lane max-heap holds (key, index) with key = the FP64 dist_sq rounded up to FP32
+// (8 bytes per entry instead of 12, so more warps fit in shared memory).  ru() is monotone, so
+// different keys order exactly like the FP64 values; equal keys are resolved by recomputing both
+// FP64 distances from the coordinates (the reference expression) and then the index.
+__device__ __noinline__ bool key_tie_after(u32 ia, u32 ib, const double* __restrict__ px,
+                                           const double* __restrict__ py, const double* __restrict__ pz,
+                                           double cx, double cy, double cz) {
+    if (ia == ib) return false;
+    const double da = point_dist_sq(px[ia], py[ia], pz[ia], cx, cy, cz);
+    const double db = point_dist_sq(px[ib], py[ib], pz[ib], cx, cy, cz);
+    return da > db || (da == db && ia > ib);
+}
+
+struct KeyHeap {
+    float* hk;
+    u32* hi;
+    u32 size;
+    const double* __restrict__ px;
+    const double* __restrict__ py;
+    const double* __restrict__ pz;
+    double cx, cy, cz;
+
+    // (ka, ia) after (kb, ib) in (dist_sq, index) order; the rare equal-key case is out of line
+    // so its coordinate loads are never hoisted into the common path
+    __device__ __forceinline__ bool after(float ka, u32 ia, float kb, u32 ib) const {
+        if (ka != kb) return ka > kb;
+        return key_tie_after(ia, ib, px, py, pz, cx, cy, cz);
+    }
+    __device__ __forceinline__ void push(float k, u32 i) {
+        u32 pos = size++;
+        while (pos > 0) {
+            const u32 par = (pos - 1) >> 1;
+            const float pk = hk[par * 32];
+            const u32 pi = hi[par * 32];
+            if (!after(k, i, pk, pi)) break;
+            hk[pos * 32] = pk;
+            hi[pos * 32] = pi;
+            pos = par;
+        }
+        hk[pos * 32] = k;
+        hi[pos * 32] = i;
+    }
+    __device__ __forceinline__ void sift_down(float k, u32 i, u32 n) {
+        u32 pos = 0;
+        for (;;) {
+            u32 c = 2 * pos + 1;
+            if (c >= n) break;
+            float ck = hk[c * 32];
+            u32 ci = hi[c * 32];
+            if (c + 1 < n) {
+                const float rk = hk[(c + 1) * 32];
+                const u32 ri = hi[(c + 1) * 32];
+                if (after(rk, ri, ck, ci)) c = c + 1, ck = rk, ci = ri;
+            }
+            if (!after(ck, ci, k, i)) break;
+            hk[pos * 32] = ck;
+            hi[pos * 32] = ci;
+            pos = c;
+        }
+        hk[pos * 32] = k;
+        hi[pos * 32] = i;
+    }
+    template <int LOGK>
+    __device__ __forceinline__ void sift_down_fixed(float k, u32 i) {
+        constexpr u32 n = 1u << LOGK;
+        u32 pos = 0;
+#pragma unroll
+        for (int lv = 0; lv < LOGK; ++lv) {
+            u32 c = 2 * pos + 1;
+            if (c >= n) break;
+            float ck = hk[c * 32];
+            u32 ci = hi[c * 32];
+            if (c + 1 < n) {
+                const float rk = hk[(c + 1) * 32];
+                const u32 ri = hi[(c + 1) * 32];
+                if (after(rk, ri, ck, ci)) c = c + 1, ck = rk, ci = ri;
+            }
+            if (!after(ck, ci, k, i)) break;
+            hk[pos * 32] = ck;
+            hi[pos * 32] = ci;
+            pos = c;
+        }
+        hk[pos * 32] = k;
+        hi[pos * 32] = i;
+    }
+};
+
 // One candidate j (global index g, FP32 squared distance v) for this lane.
-template <int KC>
-__device__ __forceinline__ void knn_offer(LaneHeap& heap, u32 k, double& worst_d, u32& worst_i,
+template <class Heap>
+__device__ __forceinline__ Heap make_heap(typename std::conditional_t<std::is_same_v<Heap, KeyHeap>, float, double>* hd,
+                                          u32* hi, const double* px, const double* py, const double* pz,
+                                          double cx, double cy, double cz) {
+    if constexpr (std::is_same_v<Heap, KeyHeap>) return KeyHeap{hd, hi, 0, px, py, pz, cx, cy, cz};
+    else return LaneHeap{hd, hi, 0};
+}
+
+// Heap keys: LaneHeap keeps the exact FP64 dist_sq (12-byte entries), KeyHeap its FP32
+// round-up (8-byte entries, more resident warps; chosen for k >= 32).
+__device__ __forceinline__ double heap_key(const LaneHeap&, double d) { return d; }
+__device__ __forceinline__ float heap_key(const KeyHeap&, double d) { return __double2float_ru(d); }
+__device__ __forceinline__ double heap_root(const LaneHeap& h) { return h.hd[0]; }
+__device__ __forceinline__ float heap_root(const KeyHeap& h) { return h.hk[0]; }
+
+template <int KC, class Heap, class Key>
+__device__ __forceinline__ void knn_offer(Heap& heap, u32 k, Key& worst_k, u32& worst_i,
                                           float& T, float E, float v, u32 g, double cx, double cy,
                                           double cz, const double* pxyz) {
     if (v > T) return;
     const double d = point_dist_sq(pxyz[0], pxyz[1], pxyz[2], cx, cy, cz);
+    const Key kd = heap_key(heap, d);
     if (heap.size < k) {
-        heap.push(d, g);
+        heap.push(kd, g);
         if (heap.size == k) {
-            worst_d = heap.hd[0];
+            worst_k = heap_root(heap);
             worst_i = heap.hi[0];
-            T = knn_threshold(worst_d, E);
+            T = knn_threshold(static_cast<double>(worst_k), E);  // a key >= the exact worst: safe
         }
-    } else if (after(worst_d, worst_i, d, g)) {
-        if constexpr (KC == 8) heap.sift_down_fixed<3>(d, g);
-        else if constexpr (KC == 16) heap.sift_down_fixed<4>(d, g);
-        else if constexpr (KC == 32) heap.sift_down_fixed<5>(d, g);
-        else if constexpr (KC == 64) heap.sift_down_fixed<6>(d, g);
-        else heap.sift_down(d, g, k);
-        worst_d = heap.hd[0];
+    } else if (heap.after(worst_k, worst_i, kd, g)) {
+        if constexpr (KC == 8) heap.template sift_down_fixed<3>(kd, g);
+        else if constexpr (KC == 16) heap.template sift_down_fixed<4>(kd, g);
+        else if constexpr (KC == 32) heap.template sift_down_fixed<5>(kd, g);
+        else if constexpr (KC == 64) heap.template sift_down_fixed<6>(kd, g);
+        else heap.sift_down(kd, g, k);
+        worst_k = heap_root(heap);
         worst_i = heap.hi[0];
-        T = knn_threshold(worst_d, E);
+        T = knn_threshold(static_cast<double>(worst_k), E);
     }
 }
 
 // Tests the `cnt` staged candidates against this lane's query (pairs, packed FP32).
-template <int KC>
+template <int KC, class Heap, class Key>
 __device__ __forceinline__ void knn_chunk(const KnnSmem& S, u32 cnt, bool active, u64 QX, u64 QY,
-                                          u64 QZ, LaneHeap& heap, u32 k, double& worst_d,
+                                          u64 QZ, Heap& heap, u32 k, Key& worst_d,
                                           u32& worst_i, float& T, float E, double cx, double cy,
                                           double cz, u32 skip_lo, u32 skip_hi) {
     if (!active) return;
@@ -137,14 +242,16 @@ __device__ __forceinline__ void knn_stage(const KnnSmem& S, const float4* __rest
 constexpr int kKnnFloatStack = kStackCap;
 constexpr i64 kSeedSortedIdx = -2;  // seed_base: queries are ascending cloud indices (q.idx)
 
-template <bool GLOBAL_HEAP, int KC>
+template <bool GLOBAL_HEAP, int KC, bool KEYED>
 __global__ void __launch_bounds__(128) knn_float_kernel(
     const TNodeF* __restrict__ tf, const float4* __restrict__ pf, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, u64 npoints, Queries q,
     i64 seed_base, u32 seed_half, float E, u32 k_in, u32* __restrict__ out_idx,
-    double* __restrict__ out_dist, double* __restrict__ gheap_d, u32* __restrict__ gheap_i,
+    double* __restrict__ out_dist, void* __restrict__ gheap_d, u32* __restrict__ gheap_i,
     u64* tile_counter) {
     extern __shared__ __align__(16) unsigned char smem[];
+    using Heap = std::conditional_t<KEYED, KeyHeap, LaneHeap>;
+    using Key = std::conditional_t<KEYED, float, double>;
     const u32 k = KC > 0 ? static_cast<u32>(KC) : k_in;
     const int warps = blockDim.x >> 5;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -157,14 +264,14 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
     S.pa = reinterpret_cast<float4*>(mine + kKnnOffPa);
     S.pb = reinterpret_cast<float2*>(mine + kKnnOffPb);
     S.pidx = reinterpret_cast<u32*>(mine + kKnnOffPidx);
-    double* hd;
+    Key* hd;
     u32* hi;
     if (GLOBAL_HEAP) {
         const u64 slot = static_cast<u64>(blockIdx.x) * warps + w;
-        hd = gheap_d + slot * k * 32 + lane;
+        hd = static_cast<Key*>(gheap_d) + slot * k * 32 + lane;
         hi = gheap_i + slot * k * 32 + lane;
     } else {
-        double* heaps_d = reinterpret_cast<double*>(smem + warps * kKnnFixed);
+        Key* heaps_d = reinterpret_cast<Key*>(smem + warps * kKnnFixed);
         u32* heaps_i = reinterpret_cast<u32*>(heaps_d + static_cast<u64>(warps) * k * 32);
         hd = heaps_d + static_cast<u64>(w) * k * 32 + lane;
         hi = heaps_i + static_cast<u64>(w) * k * 32 + lane;
@@ -185,8 +292,8 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
             qf = load_query_f(q, qi);
         }
         const u64 QX = pack2(qf.x, qf.x), QY = pack2(qf.y, qf.y), QZ = pack2(qf.z, qf.z);
-        LaneHeap heap{hd, hi, 0};
-        double worst_d = 0.0;
+        Heap heap = make_heap<Heap>(hd, hi, px, py, pz, cx, cy, cz);
+        Key worst_d = 0;
         u32 worst_i = 0;
         float T = active ? INFINITY : -INFINITY;  // inactive lanes want nothing
         __syncwarp();
@@ -297,9 +404,9 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
         if (active) {
             const u32 n = heap.size;
             for (u32 e = n; e > 1; --e) {
-                const double td = hd[0];
+                const Key td = hd[0];
                 const u32 ti = hi[0];
-                const double ld = hd[(e - 1) * 32];
+                const Key ld = hd[(e - 1) * 32];
                 const u32 li = hi[(e - 1) * 32];
                 hd[(e - 1) * 32] = td;
                 hi[(e - 1) * 32] = ti;
@@ -310,13 +417,19 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
         const u64 left = q.m - tile * 32;
         const u32 nact = left < 32 ? static_cast<u32>(left) : 32u;
         for (u32 L = 0; L < nact; ++L) {
+            // the row's FP64 distances are recomputed with the reference expression
+            const double qx = __shfl_sync(~0u, cx, L), qy = __shfl_sync(~0u, cy, L), qz = __shfl_sync(~0u, cz, L);
             u32* oi = out_idx + (tile * 32 + L) * k;
             double* od = out_dist + (tile * 32 + L) * k;
-            const double* rhd = hd - lane + L;
             const u32* rhi = hi - lane + L;
+            const Key* rhd = hd - lane + L;
             for (u32 e = lane; e < k; e += 32) {
-                oi[e] = rhi[e * 32];
-                od[e] = rhd[e * 32];
+                const u32 j = rhi[e * 32];
+                oi[e] = j;
+                if constexpr (KEYED)
+                    od[e] = point_dist_sq(__ldg(px + j), __ldg(py + j), __ldg(pz + j), qx, qy, qz);
+                else
+                    od[e] = rhd[e * 32];
             }
         }
         __syncwarp();
