@@ -132,13 +132,14 @@ __global__ void __launch_bounds__(kScanThreads) scan_tile_sums(const In* in, u64
     if (threadIdx.x == 0) sums[blockIdx.x] = s;
 }
 
-__global__ void __launch_bounds__(1024) scan_sums(u64* sums, int nb, u64* total_out) {
-    using BlockScan = cub::BlockScan<u64, 1024>;
+constexpr int kSumsThreads = 256;
+__global__ void __launch_bounds__(kSumsThreads) scan_sums(u64* sums, int nb, u64* total_out) {
+    using BlockScan = cub::BlockScan<u64, kSumsThreads>;
     __shared__ typename BlockScan::TempStorage tmp;
     __shared__ u64 carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    for (int base = 0; base < nb; base += 1024) {
+    for (int base = 0; base < nb; base += kSumsThreads) {
         const int j = base + threadIdx.x;
         const u64 v = j < nb ? sums[j] : 0;
         u64 ex, agg;
@@ -209,7 +210,7 @@ static void exclusive_scan(lo_context* ctx, const In* in, Out* out, u64 n) {
     } else {
         LO_CUDA(cudaMemsetAsync(sums, 0, sizeof(u64), ctx->stream));
     }
-    scan_sums<<<1, 1024, 0, ctx->stream>>>(sums, n > 0 ? nb : 1, sums + nb);
+    scan_sums<<<1, kSumsThreads, 0, ctx->stream>>>(sums, n > 0 ? nb : 1, sums + nb);
     LO_CHECK_LAUNCH();
     if (n > 0) {
         scan_tiles<In, Out><<<nb, kScanThreads, 0, ctx->stream>>>(in, n, sums, out);
