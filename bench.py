@@ -367,11 +367,14 @@ def run_ours(args, cfg):
             _lib.check(L.lo_host_alloc_pinned(24 * n, C.byref(pinned)))
             C.memmove(pinned, xyz_host.ctypes.data, 24 * n)
         rows = b1 - b0
-        # one pinned (counts, digests) pair per radius: radius i's results travel on the copy
-        # stream while radius i + 1 computes (lo_csr_download_async)
-        hc = [C.c_void_p() for _ in radii]
-        hf = [C.c_void_p() for _ in radii]
-        for a, b in zip(hc, hf):
+        # one pinned (counts, digests) pair per radius and step parity: radius i's results travel
+        # on the copy stream while radius i + 1 computes (lo_csr_download_async), and step s's
+        # last results land while step s + 1 starts; step s + 2 waits for them (lo_d2h_wait)
+        # before reusing their host buffers
+        per_step_sync = os.environ.get("LO_BENCH_E2E_SYNC") is not None
+        hc = [[C.c_void_p() for _ in radii] for _ in range(2)]
+        hf = [[C.c_void_p() for _ in radii] for _ in range(2)]
+        for a, b in zip(hc[0] + hc[1], hf[0] + hf[1]):
             _lib.check(L.lo_host_alloc_pinned(4 * max(rows, 1), C.byref(a)))
             _lib.check(L.lo_host_alloc_pinned(8 * max(rows, 1), C.byref(b)))
 
@@ -398,15 +401,18 @@ def run_ours(args, cfg):
                     _lib.check(L.lo_octree_build(ctx.h, coded, cfg["n_max"], C.byref(tree)))
                 if world > 1:
                     coded, tree, _, _ = D.broadcast_structure(ctx, coded, tree, src=0)
+                if s >= 2:
+                    _lib.check(L.lo_d2h_wait(ctx.h, cur))  # step s - 2's results are on the host
                 for i, r in enumerate(radii):
                     csr = C.c_void_p()
                     _lib.check(L.lo_radius_range(ctx.h, tree, coded, 1, 0, r, b0, b1, 1, C.byref(csr)))
-                    _lib.check(L.lo_csr_download_async(ctx.h, csr, hc[i], hf[i], None, None))
+                    _lib.check(L.lo_csr_download_async(ctx.h, csr, hc[cur][i], hf[cur][i], None, None))
                     L.lo_csr_destroy(csr)
+                _lib.check(L.lo_d2h_fence(ctx.h, cur))
                 free(coded, tree)
-                # each step ends with its counts + digests on the host (letting them trail into the
-                # next step measured slower: the deferred result buffers grow the memory pool)
-                _lib.check(L.lo_context_synchronize(ctx.h))
+                if per_step_sync:
+                    _lib.check(L.lo_context_synchronize(ctx.h))
+            _lib.check(L.lo_context_synchronize(ctx.h))  # every step's results on the host
 
         e2e_run(max(2, args.warmup // 2))
         e0 = torch.cuda.Event(enable_timing=True)
@@ -427,12 +433,13 @@ def run_ours(args, cfg):
                "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": len(radii) * 12 * n,
                "path": "lo_h2d_begin(pinned cloud, next step's upload overlapped) -> lo_reorder_device -> "
                        "lo_octree_build -> lo_radius_range(+FNV) -> lo_csr_download_async(counts, digests; "
-                       "overlapped with the next radius) -> lo_context_synchronize"}
+                       "overlapped with the next radius and step; host buffers double-buffered behind "
+                       "lo_d2h_fence/lo_d2h_wait) -> lo_context_synchronize"}
         if rank == 0:
             L.lo_host_free_pinned(pinned)
             for d in dev_in:
                 L.lo_device_free(ctx.h, d)
-        for a, b in zip(hc, hf):
+        for a, b in zip(hc[0] + hc[1], hf[0] + hf[1]):
             L.lo_host_free_pinned(a)
             L.lo_host_free_pinned(b)
 

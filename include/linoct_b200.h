@@ -113,6 +113,12 @@ int lo_memcpy_h2d(lo_context* ctx, void* dst_dev, const void* src_host, uint64_t
  * lo_h2d_wait + lo_reorder_device on it.  slot in [0, 4). */
 int lo_h2d_begin(lo_context* ctx, void* dst_dev, const void* src_host, uint64_t bytes, int slot);
 int lo_h2d_wait(lo_context* ctx, int slot);
+/* Result fences for pipelined callers: lo_d2h_fence(slot) marks every lo_csr_download_async
+ * enqueued so far; lo_d2h_wait(slot) blocks the host until those copies have
+ * landed -- e.g. double-buffered host results: wait on slot s % 2 before reusing its buffers, fence
+ * it after the batch's downloads.  slot in [0, 4). */
+int lo_d2h_fence(lo_context* ctx, int slot);
+int lo_d2h_wait(lo_context* ctx, int slot);
 int lo_memcpy_d2h(lo_context* ctx, void* dst_host, const void* src_dev, uint64_t bytes);
 int lo_host_alloc_pinned(uint64_t bytes, void** out_host);
 int lo_host_free_pinned(void* host);

@@ -80,6 +80,8 @@ SIGNATURES = {
     "lo_csr_download_async": (cint, [P, P, P, P, P, P]),
     "lo_h2d_begin": (cint, [P, P, P, u64, cint]),
     "lo_h2d_wait": (cint, [P, cint]),
+    "lo_d2h_fence": (cint, [P, cint]),
+    "lo_d2h_wait": (cint, [P, cint]),
     "lo_csr_destroy": (cint, [P]),
     "lo_csr_struct_info": (cint, [P, P, P]),
     "lo_reorder_pcb": (cint, [P, C.c_char_p, cint, cint, PP]),

@@ -171,6 +171,11 @@ static void unsort_csr_part(lo_context* ctx, const SortedCentres& s, u64 m, u64*
 
 void unsort_csr(lo_context* ctx, const SortedCentres& s, lo_csr* c) {
     const u64 m = c->rows;
+    if (c->digested) {  // the row digests are still being computed on the aux stream
+        LO_CUDA(cudaStreamWaitEvent(ctx->stream, c->digested, 0));
+        cudaEventDestroy(c->digested);
+        c->digested = nullptr;
+    }
     if (m == 0) return;
     stage_begin(ctx, "centre_unsort");
     u32* counts = dalloc_t<u32>(ctx, m);
@@ -195,6 +200,7 @@ void unsort_csr(lo_context* ctx, const SortedCentres& s, lo_csr* c) {
     } else {
         unsort_csr_part(ctx, s, m, c->offsets, c->indices, c->total, 1);
     }
+    for (auto& b : c->cap) b = 0;  // replaced (or stream-ordered) buffers: plain frees from here on
     stage_end(ctx);
     sync(ctx);
 }

@@ -44,10 +44,94 @@ void reclaim(lo_context* ctx, bool wait) {
     }
 }
 
+constexpr size_t kBigBytes = 64ull << 20;  // buffers from this size go through the cache
+constexpr size_t kCacheEntries = 16;
+
+static bool cache_ready(const lo_context::Cached& c) {
+    if (!c.ready) return true;  // last used on ctx->stream: stream order makes it reusable
+    if (cudaEventQuery(c.ready) == cudaSuccess) return true;
+    cudaGetLastError();  // cudaErrorNotReady is not an error
+    return false;
+}
+
+static void cache_free(lo_context* ctx, lo_context::Cached& c) {
+    if (c.ready) {
+        cudaEventSynchronize(c.ready);
+        cudaEventDestroy(c.ready);
+    }
+    cudaFreeAsync(c.p, ctx->stream);
+}
+
+void* big_alloc(lo_context* ctx, size_t bytes, size_t* got) {
+    *got = bytes;
+    if (bytes >= kBigBytes) {
+        auto& c = ctx->cache;
+        int best = -1;
+        for (size_t i = 0; i < c.size(); ++i) {
+            if (c[i].bytes < bytes || c[i].bytes > bytes + bytes / 2 + kBigBytes) continue;
+            if (!cache_ready(c[i])) continue;
+            if (best < 0 || c[i].bytes < c[best].bytes) best = static_cast<int>(i);
+        }
+        if (best >= 0) {
+            void* p = c[best].p;
+            *got = c[best].bytes;
+            if (c[best].ready) cudaEventDestroy(c[best].ready);
+            c.erase(c.begin() + best);
+            return p;
+        }
+    }
+    return dalloc(ctx, bytes);
+}
+
+void big_release(lo_context* ctx, void* p, size_t bytes, cudaStream_t last_use) {
+    if (!p) return;
+    if (bytes < kBigBytes) {
+        if (last_use == ctx->stream) {
+            dfree(ctx, p);
+        } else {  // release once the other stream's reader has finished
+            lo_context::Deferred d{nullptr, {p}};
+            LO_CUDA(cudaEventCreateWithFlags(&d.done, cudaEventDisableTiming));
+            LO_CUDA(cudaEventRecord(d.done, last_use));
+            ctx->deferred.push_back(std::move(d));
+        }
+        return;
+    }
+    lo_context::Cached c{p, bytes, nullptr};
+    if (last_use != ctx->stream) {
+        LO_CUDA(cudaEventCreateWithFlags(&c.ready, cudaEventDisableTiming));
+        LO_CUDA(cudaEventRecord(c.ready, last_use));
+    }
+    auto& cache = ctx->cache;
+    cache.push_back(c);
+    // over the limit the oldest finished buffers go back to the pool (waiting only if none has)
+    for (size_t i = 0; i < cache.size() && cache.size() > kCacheEntries;) {
+        if (cache_ready(cache[i])) {
+            cache_free(ctx, cache[i]);
+            cache.erase(cache.begin() + i);
+        } else {
+            ++i;
+        }
+    }
+    while (cache.size() > 2 * kCacheEntries) {
+        cache_free(ctx, cache.front());
+        cache.erase(cache.begin());
+    }
+}
+
+void cache_drain(lo_context* ctx) {
+    for (auto& c : ctx->cache) cache_free(ctx, c);
+    ctx->cache.clear();
+}
+
 void* dalloc(lo_context* ctx, size_t bytes) {
     if (!ctx->deferred.empty()) reclaim(ctx, false);
     void* p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, bytes, ctx->stream);
+    if (e != cudaSuccess && !ctx->cache.empty()) {  // parked buffers go back first
+        cudaGetLastError();
+        cache_drain(ctx);
+        e = cudaMallocAsync(&p, bytes, ctx->stream);
+    }
     if (e != cudaSuccess) {
         cudaGetLastError();
         char buf[160];
@@ -379,7 +463,9 @@ int lo_context_create(int device, void* stream, lo_context** out) {
         }
         LO_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         LO_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+        LO_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
         for (auto& e : ctx->h2d_done) LO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : ctx->d2h_done) LO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         cudaMemPool_t pool;
         LO_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
         u64 threshold = ~0ull;
@@ -395,14 +481,19 @@ int lo_context_destroy(lo_context* ctx) {
         if (!ctx) return;
         cudaStreamSynchronize(ctx->stream);
         if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+        if (ctx->aux_stream) cudaStreamSynchronize(ctx->aux_stream);
         reclaim(ctx, true);
+        cache_drain(ctx);
         cudaStreamSynchronize(ctx->stream);
         if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+        if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
         if (ctx->h2d_stream) {
             cudaStreamSynchronize(ctx->h2d_stream);
             cudaStreamDestroy(ctx->h2d_stream);
         }
         for (auto& e : ctx->h2d_done)
+            if (e) cudaEventDestroy(e);
+        for (auto& e : ctx->d2h_done)
             if (e) cudaEventDestroy(e);
         for (auto& s : ctx->stages) {
             cudaEventDestroy(s.a);
@@ -420,6 +511,7 @@ int lo_context_synchronize(lo_context* ctx) {
         sync(ctx);
         LO_CUDA(cudaStreamSynchronize(ctx->copy_stream));
         LO_CUDA(cudaStreamSynchronize(ctx->h2d_stream));
+        LO_CUDA(cudaStreamSynchronize(ctx->aux_stream));
         reclaim(ctx, true);
     });
 }
@@ -479,6 +571,19 @@ int lo_h2d_wait(lo_context* ctx, int slot) {
     return api([&] {
         require(slot >= 0 && slot < lo_context::kH2dSlots, LO_INVALID_ARGUMENT, "h2d slot out of range");
         LO_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->h2d_done[slot], 0));
+    });
+}
+int lo_d2h_fence(lo_context* ctx, int slot) {
+    return api([&] {
+        require(slot >= 0 && slot < lo_context::kH2dSlots, LO_INVALID_ARGUMENT, "d2h slot out of range");
+        LO_CUDA(cudaEventRecord(ctx->d2h_done[slot], ctx->copy_stream));
+    });
+}
+int lo_d2h_wait(lo_context* ctx, int slot) {
+    return api([&] {
+        require(slot >= 0 && slot < lo_context::kH2dSlots, LO_INVALID_ARGUMENT, "d2h slot out of range");
+        LO_CUDA(cudaEventSynchronize(ctx->d2h_done[slot]));
+        reclaim(ctx, false);
     });
 }
 int lo_memcpy_d2h(lo_context* ctx, void* dst, const void* src, uint64_t bytes) {

@@ -116,8 +116,20 @@ struct lo_context {
     // staged input uploads (lo_h2d_begin / lo_h2d_wait): their own stream so an upload for the
     // next batch overlaps this batch's kernels and the D2H copies; one event per slot
     cudaStream_t h2d_stream = nullptr;
+    // row digests run here, behind the fill, so the caller's next batch can start its count pass
+    cudaStream_t aux_stream = nullptr;
+    // large result buffers released while another stream may still read them are parked here
+    // with an event and reused (or freed) once it has completed -- the stream-ordered pool
+    // handles cross-stream frees of multi-GB buffers badly (it grows instead of reusing)
+    struct Cached {
+        void* p;
+        size_t bytes;
+        cudaEvent_t ready;
+    };
+    std::vector<Cached> cache;
     static constexpr int kH2dSlots = 4;
     cudaEvent_t h2d_done[kH2dSlots] = {};
+    cudaEvent_t d2h_done[kH2dSlots] = {};  // lo_d2h_fence / lo_d2h_wait
 };
 
 struct lo_coded {
@@ -181,7 +193,10 @@ struct lo_csr {
     lo::u64* single_offsets = nullptr;  // [rows+1]
     lo::u32* singles = nullptr;         // [total_singles]
     cudaEvent_t copied = nullptr;       // last lo_csr_download_async (null: none pending)
+    cudaEvent_t digested = nullptr;     // digests computed on the aux stream (null: inline / none)
     unsigned copy_mask = 0;             // buffers it reads: 1 counts, 2 fps, 4 offsets, 8 indices
+    // block sizes of counts / fps / offsets / indices when they came from big_alloc (0: dalloc)
+    size_t cap[4] = {0, 0, 0, 0};
 };
 
 namespace lo {
@@ -229,6 +244,15 @@ namespace lo {
 
 // ---- memory + timing helpers (context.cu) ------------------------------------------------
 void* dalloc(lo_context* ctx, size_t bytes);
+// Large buffers through the context's cache: reuse a parked buffer whose last reader finished,
+// else allocate; release parks it behind an event recorded on `last_use`.
+void* big_alloc(lo_context* ctx, size_t bytes, size_t* got);
+template <class T>
+T* big_alloc_t(lo_context* ctx, u64 n, size_t* got) {
+    return static_cast<T*>(big_alloc(ctx, n ? n * sizeof(T) : 16, got));
+}
+void big_release(lo_context* ctx, void* p, size_t bytes, cudaStream_t last_use);
+void cache_drain(lo_context* ctx);
 // Releases deferred buffers whose async copies finished (all of them when wait is true).
 void reclaim(lo_context* ctx, bool wait);
 void dfree(lo_context* ctx, void* p);

@@ -201,8 +201,8 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
     u32* ovf_n = nullptr;
     try {
         LO_CUDA(cudaEventRecord(e0, ctx->stream));
-        out->counts = dalloc_t<u32>(ctx, q.m);
-        out->offsets = dalloc_t<u64>(ctx, q.m + 1);
+        out->counts = big_alloc_t<u32>(ctx, q.m, &out->cap[0]);
+        out->offsets = big_alloc_t<u64>(ctx, q.m + 1, &out->cap[2]);
         const u64 tiles = (q.m + 31) / 32;
         static const bool no_fuse = std::getenv("LO_RADIUS_NO_FUSE") != nullptr;
         if (q.m && !no_fuse && float_path(t, c, q, r)) {
@@ -223,7 +223,7 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
         exclusive_scan_u32_to_u64(ctx, out->counts, out->offsets, q.m);
         stage_end(ctx);
         out->total = read_scalar(ctx, out->offsets + q.m);
-        out->indices = dalloc_t<u32>(ctx, out->total);
+        out->indices = big_alloc_t<u32>(ctx, out->total, &out->cap[3]);
         stage_begin(ctx, "radius_fill");
         if (q.m && ra.rp.pool) {
             const u32 n_ovf = replay_records(ctx, RecSetup{ra.rp, ovf, ovf_n}, q.m, out->offsets,
@@ -244,24 +244,33 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
         stage_end(ctx);
         ra = RecArgs{};
         ovf = ovf_n = nullptr;
-        if (fingerprint) {
-            out->fps = dalloc_t<u64>(ctx, q.m);
-            stage_begin(ctx, "radius_digest");
-            if (q.m)
-                radius_digest<<<std::max(1, ceil_div(q.m, 256)), 256, 0, ctx->stream>>>(
-                    out->offsets, out->indices, q.m, out->fps);
-            LO_CHECK_LAUNCH();
-            stage_end(ctx);
-        }
         LO_CUDA(cudaEventRecord(e1, ctx->stream));
-        sync(ctx);
+        if (fingerprint) {
+            out->fps = big_alloc_t<u64>(ctx, q.m, &out->cap[1]);
+            if (q.m && !ctx->timing) {
+                // the digests trail on the aux stream while the caller's next batch counts;
+                // readers of fps / indices (downloads, unsort, release) order behind `digested`
+                LO_CUDA(cudaStreamWaitEvent(ctx->aux_stream, e1, 0));
+                LO_CUDA(cudaEventCreateWithFlags(&out->digested, cudaEventDisableTiming));
+                radius_digest<<<std::max(1, ceil_div(q.m, 256)), 256, 0, ctx->aux_stream>>>(
+                    out->offsets, out->indices, q.m, out->fps);
+                LO_CHECK_LAUNCH();
+                LO_CUDA(cudaEventRecord(out->digested, ctx->aux_stream));
+            } else {
+                stage_begin(ctx, "radius_digest");
+                if (q.m)
+                    radius_digest<<<std::max(1, ceil_div(q.m, 256)), 256, 0, ctx->stream>>>(
+                        out->offsets, out->indices, q.m, out->fps);
+                LO_CHECK_LAUNCH();
+                stage_end(ctx);
+                LO_CUDA(cudaEventRecord(e1, ctx->stream));
+            }
+        }
+        LO_CUDA(cudaEventSynchronize(e1));
         LO_CUDA(cudaEventElapsedTime(&out->ms, e0, e1));
         out->mean = q.m ? static_cast<double>(out->total) / static_cast<double>(q.m) : 0.0;
     } catch (...) {
-        dfree(ctx, out->counts);
-        dfree(ctx, out->offsets);
-        dfree(ctx, out->indices);
-        dfree(ctx, out->fps);
+        free_csr_buffers(ctx, out);
         delete out;
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
@@ -420,6 +429,7 @@ int lo_csr_info_get(const lo_csr* csr, lo_csr_info* out) {
 int lo_csr_download(lo_context* ctx, const lo_csr* csr, uint32_t* counts_host,
                     uint64_t* fingerprints_host, uint64_t* offsets_host, uint32_t* indices_host) {
     return api([&] {
+        if (csr->digested) LO_CUDA(cudaStreamWaitEvent(ctx->stream, csr->digested, 0));
         if (counts_host && csr->rows)
             LO_CUDA(cudaMemcpyAsync(counts_host, csr->counts, 4 * csr->rows, cudaMemcpyDeviceToHost,
                                     ctx->stream));
@@ -452,6 +462,7 @@ int lo_csr_download_async(lo_context* ctx, lo_csr* csr, uint32_t* counts_host,
         LO_CUDA(cudaEventRecord(ready, ctx->stream));
         LO_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
         cudaEventDestroy(ready);  // released once the recorded work completes
+        if (csr->digested) LO_CUDA(cudaStreamWaitEvent(ctx->copy_stream, csr->digested, 0));
         cudaStream_t s = ctx->copy_stream;
         csr->copy_mask |= (counts_host ? 1u : 0u) | (fingerprints_host ? 2u : 0u) | (offsets_host ? 4u : 0u) |
                           (indices_host ? 8u : 0u);

@@ -691,35 +691,47 @@ void ensure_expanded(lo_context* ctx, lo_csr* csr) {
     LO_CHECK_LAUNCH();
 }
 
+// Releases a result's buffers in order behind their last reader: a pending async download
+// (whose stream waited for the digests), else pending digests on the aux stream, else ctx->stream.
+// Buffers from big_alloc are parked in the context cache; the rest are freed (deferred if guarded).
 void free_csr_buffers(lo_context* ctx, lo_csr* csr) {
-    if (csr->copied) {
-        if (cudaEventQuery(csr->copied) != cudaSuccess) {
-            // an async download still reads some buffers: release those once it has finished
-            cudaGetLastError();
-            lo_context::Deferred d{csr->copied, {}};
-            void** bufs[4] = {reinterpret_cast<void**>(&csr->counts), reinterpret_cast<void**>(&csr->fps),
-                              reinterpret_cast<void**>(&csr->offsets), reinterpret_cast<void**>(&csr->indices)};
-            for (int b = 0; b < 4; ++b)
-                if ((csr->copy_mask >> b) & 1u && *bufs[b]) {
-                    d.ptrs.push_back(*bufs[b]);
-                    *bufs[b] = nullptr;
-                }
-            ctx->deferred.push_back(std::move(d));
-        } else {
-            cudaEventDestroy(csr->copied);
-        }
-        csr->copied = nullptr;
-        csr->copy_mask = 0;
+    auto pending = [](cudaEvent_t& e) {
+        if (!e) return false;
+        const bool busy = cudaEventQuery(e) != cudaSuccess;
+        if (busy) cudaGetLastError();  // cudaErrorNotReady is not an error
+        cudaEventDestroy(e);  // released once recorded work completes
+        e = nullptr;
+        return busy;
+    };
+    cudaStream_t last = ctx->stream;
+    unsigned guarded = 0;
+    if (pending(csr->copied)) {
+        last = ctx->copy_stream;
+        guarded = csr->copy_mask | 2u | 4u | 8u;  // the copy stream also waited for the digests
     }
-    dfree(ctx, csr->counts);
-    dfree(ctx, csr->offsets);
-    dfree(ctx, csr->indices);
-    dfree(ctx, csr->fps);
+    if (pending(csr->digested) && !guarded) {
+        last = ctx->aux_stream;
+        guarded = 2u | 4u | 8u;  // fps, offsets, indices
+    }
+    csr->copy_mask = 0;
+    void** bufs[4] = {reinterpret_cast<void**>(&csr->counts), reinterpret_cast<void**>(&csr->fps),
+                      reinterpret_cast<void**>(&csr->offsets), reinterpret_cast<void**>(&csr->indices)};
+    for (int b = 0; b < 4; ++b) {
+        if (!*bufs[b]) continue;
+        const cudaStream_t s = (guarded >> b) & 1u ? last : ctx->stream;
+        if (csr->cap[b])
+            big_release(ctx, *bufs[b], csr->cap[b], s);
+        else if (s == ctx->stream)
+            dfree(ctx, *bufs[b]);
+        else
+            big_release(ctx, *bufs[b], 0, s);  // deferred behind the reader
+        *bufs[b] = nullptr;
+        csr->cap[b] = 0;
+    }
     dfree(ctx, csr->range_offsets);
     dfree(ctx, csr->ranges);
     dfree(ctx, csr->single_offsets);
     dfree(ctx, csr->singles);
-    csr->counts = nullptr, csr->offsets = nullptr, csr->indices = nullptr, csr->fps = nullptr;
     csr->range_offsets = nullptr, csr->ranges = nullptr, csr->single_offsets = nullptr;
     csr->singles = nullptr;
 }

@@ -43,3 +43,41 @@ def test_async_download_overlaps_and_matches(ctx, oracle):
         _lib.check(L.lo_context_synchronize(ctx.h))
         for (counts, fps), w in zip(got, want):
             assert np.array_equal(counts, w.counts) and np.array_equal(fps, w.fingerprints)
+
+
+def test_pipelined_steps_with_d2h_fences(ctx, oracle):
+    """Three steps whose results trail into the next step (digests on the aux stream, copies on the
+    copy stream, result buffers parked in the context cache), host buffers double-buffered behind
+    lo_d2h_fence / lo_d2h_wait: every step's counts and digests equal the synchronous ones."""
+    pts = oracle.gen_terrain(300000, 5, 200.0)
+    coded = lo.reorder_cloud(pts, lo.Curve.Hilbert)
+    tree = lo.LinearOctree(coded, 32)
+    L = _lib.lib()
+    n = coded.n
+    radii = [1.0, 3.0]
+    want = [lo.run_radius_batch(tree, coded, lo.RadiusMethod.Lin, lo.KernelShape.Sphere, r, lo.BatchOptions())
+            for r in radii]
+    host = [[(np.zeros(n, np.uint32), np.zeros(n, np.uint64)) for _ in radii] for _ in range(2)]
+    seen = 0
+    for s in range(4):
+        cur = s % 2
+        if s >= 2:
+            _lib.check(L.lo_d2h_wait(ctx.h, cur))
+            for (counts, fps), w in zip(host[cur], want):
+                assert np.array_equal(counts, w.counts) and np.array_equal(fps, w.fingerprints)
+                counts[:] = 0
+                fps[:] = 0
+            seen += 1
+        for (counts, fps), r in zip(host[cur], radii):
+            h = C.c_void_p()
+            _lib.check(L.lo_radius_range(ctx.h, tree.h, coded.h, 1, 0, r, 0, n, 1, C.byref(h)))
+            _lib.check(L.lo_csr_download_async(ctx.h, h, counts.ctypes.data, fps.ctypes.data, None, None))
+            L.lo_csr_destroy(h)
+        _lib.check(L.lo_d2h_fence(ctx.h, cur))
+    _lib.check(L.lo_context_synchronize(ctx.h))
+    for buf in host:
+        for (counts, fps), w in zip(buf, want):
+            assert np.array_equal(counts, w.counts) and np.array_equal(fps, w.fingerprints)
+    assert seen == 2
+    with pytest.raises(Exception):
+        _lib.check(L.lo_d2h_fence(ctx.h, 4))
