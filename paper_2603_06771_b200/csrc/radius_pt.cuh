@@ -14,7 +14,9 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "radius_float.cuh"
 
@@ -372,6 +374,48 @@ static inline RecSetup setup_records(lo_context* ctx, u64 tiles, u32 cap) {
     return rs;
 }
 
+// Diagnostic (LO_REPLAY_STATS): the records' shape -- records per tile, (row, record) pairs with
+// members, and the sum over records of the largest per-row member count -- printed to stderr.
+static inline void replay_stats(lo_context* ctx, const RecSetup& rs, u64 m, u64 tiles) {
+    std::vector<u32> rn(tiles);
+    std::vector<u64> ro(tiles);
+    u64 alloc = 0;
+    LO_CUDA(cudaMemcpyAsync(rn.data(), rs.rp.rec_n, 4 * tiles, cudaMemcpyDeviceToHost, ctx->stream));
+    LO_CUDA(cudaMemcpyAsync(ro.data(), rs.rp.rec_off, 8 * tiles, cudaMemcpyDeviceToHost, ctx->stream));
+    LO_CUDA(cudaMemcpyAsync(&alloc, rs.rp.alloc, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    alloc = std::min<u64>(alloc, rs.rp.pool_recs);
+    std::vector<u32> pool(alloc * 64);
+    LO_CUDA(cudaMemcpyAsync(pool.data(), rs.rp.pool, 256 * alloc, cudaMemcpyDeviceToHost, ctx->stream));
+    sync(ctx);
+    double recs = 0, pairs = 0, maxsum = 0, members = 0, used = 0;
+    u64 hist[9] = {};
+    for (u64 t = 0; t < tiles; ++t) {
+        if (rn[t] == kRecOverflow) continue;
+        used += 1;
+        recs += rn[t];
+        hist[std::min<u32>(8, rn[t] / 16)]++;
+        for (u32 b = 0; b < rn[t]; ++b) {
+            const u32* R = pool.data() + (ro[t] + b) * 64;
+            u32 mx = 0;
+            for (u32 L = 0; L < 32; ++L) {
+                const u32 c = static_cast<u32>(__builtin_popcount(R[32 + L]));
+                pairs += c != 0;
+                members += c;
+                mx = std::max(mx, c);
+            }
+            maxsum += mx;
+        }
+    }
+    std::fprintf(stderr,
+                 "[lo] replay stats: m=%llu tiles=%llu recorded=%.0f recs/tile=%.1f pairs/tile=%.1f "
+                 "members/tile=%.1f members/pair=%.2f maxpop-sum/tile=%.1f  n-hist(16s):",
+                 static_cast<unsigned long long>(m), static_cast<unsigned long long>(tiles), used, recs / used,
+                 pairs / used, members / used, members / std::max(1.0, pairs), maxsum / used);
+    for (u64 h : hist) std::fprintf(stderr, " %llu", static_cast<unsigned long long>(h));
+    std::fprintf(stderr, "\n");
+}
+
 // Fill by replaying the records into the CSR (offsets[m+1], out); returns how many tiles
 // overflowed (their ids in rs.ovf) and need the fill walk.
 static inline u32 replay_records(lo_context* ctx, const RecSetup& rs, u64 m, const u64* offsets, u32* out,
@@ -401,6 +445,8 @@ static inline u32 replay_records(lo_context* ctx, const RecSetup& rs, u64 m, con
                                                                                 rs.ovf_n);
     }
     LO_CHECK_LAUNCH();
+    static const bool stats = std::getenv("LO_REPLAY_STATS") != nullptr;
+    if (stats) replay_stats(ctx, rs, m, tiles);
     return read_scalar(ctx, rs.ovf_n);
 }
 
