@@ -28,6 +28,7 @@ constexpr int kPtThreads = 32 * kPtWarps;
 struct PtShared {
     u32 stack[kStackCap];
     float4 buf[32];      // candidate (x, y, z) relative FP32, .w = point index bits
+    u32 bix[32];         // candidate point indices, staged per leaf (loaded per buffer)
     float4 qf[32];       // queries, FP32
     __align__(16) float qx[32];  // queries, FP32 SoA: (q[2p], q[2p+1]) loads as one f32x2
     __align__(16) float qy[32];
@@ -53,7 +54,7 @@ __device__ __forceinline__ u32 band_fix(u32 in, u32 band, const PtShared& S, int
 // keeps query L's count (count pass) or its CSR cursor relative to the tile's first row
 // (fill pass) in a register.
 template <int SHAPE, bool FILL>
-__device__ __forceinline__ void process_buffer(PtShared& S, u32 fill, u32 qmask, int lane,
+__device__ __forceinline__ void process_buffer(PtShared& S, const float4 P, u32 fill, u32 qmask, int lane,
                                                float lo_thr, float hi_thr,
                                                const double* __restrict__ px,
                                                const double* __restrict__ py,
@@ -64,7 +65,6 @@ __device__ __forceinline__ void process_buffer(PtShared& S, u32 fill, u32 qmask,
     // slots >= fill hold +INF (staged that way), so they are never members; a query that is
     // disjoint from every leaf of the buffer has d2_f >= near2_f >= t_hi for all its points,
     // so testing it anyway yields an empty ballot -- no per-query interest masks are needed.
-    const float4 P = S.buf[lane];
     const u32 idx = __float_as_uint(P.w);
     const u64 PX = pack2(P.x, P.x), PY = pack2(P.y, P.y), PZ = pack2(P.z, P.z);
     const u32 lt = (1u << lane) - 1u;
@@ -520,15 +520,23 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
         u32 nrec = 0;             // count pass: buffers recorded for the replay
         u32* rec_tile = (!FILL && rp.pool && chunk_left >= rp.cap) ? rp.pool + chunk_base * 64 : nullptr;
         auto flush = [&]() {
+            // the buffer's points are loaded here, all 32 at once (one latency per buffer instead
+            // of one per leaf); slots >= fill get +INF coordinates, never members
+            float4 P = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+            if (static_cast<u32>(lane) < fill) {
+                const u32 g = S.bix[lane];
+                P = __ldg(pf + g);
+                P.w = __uint_as_float(g);
+            }
             u32 mymask = 0;
-            process_buffer<SHAPE, FILL>(S, fill, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2,
+            process_buffer<SHAPE, FILL>(S, P, fill, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2,
                                         out_tile, mine, mymask);
             if (!FILL) {
                 mine += __popc(mymask);
                 if (rec_tile) {
                     if (nrec < rp.cap) {
                         u32* R = rec_tile + nrec * 64;
-                        R[lane] = __float_as_uint(S.buf[lane].w);
+                        R[lane] = __float_as_uint(P.w);
                         R[32 + lane] = mymask;
                     }
                     ++nrec;
@@ -568,11 +576,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             for (u32 base = nd.begin; base < nd.end;) {
                 const u32 take = min(32u - fill, nd.end - base);
                 __syncwarp();
-                if (static_cast<u32>(lane) < take) {
-                    float4 p = __ldg(pf + base + lane);
-                    p.w = __uint_as_float(base + lane);
-                    S.buf[fill + lane] = p;
-                }
+                if (static_cast<u32>(lane) < take) S.bix[fill + lane] = base + lane;
                 fill += take;
                 qmask |= want;
                 base += take;
@@ -585,10 +589,8 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             }
         }
         if (fill) {
-            // partial last buffer: pad with never-member slots
-            if (static_cast<u32>(lane) >= fill) S.buf[lane] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
             __syncwarp();
-            flush();
+            flush();  // partial last buffer
         }
         if (!FILL && active) counts[qi] = mine;
         if (!FILL && rp.pool) {
