@@ -141,7 +141,14 @@ static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
     const int blocks = static_cast<int>(std::max<u64>(1, std::min<u64>((tiles + kRadiusWarps - 1) / kRadiusWarps,
                                                                       static_cast<u64>(ctx->sm_count) * 64)));
     if (float_path(t, c, q, r)) {
-        const FloatTest ft = make_float_test(r, std::max(c->bmax, q.bmax));
+        FloatTest ft = make_float_test(r, std::max(c->bmax, q.bmax));
+        // internal nodes of <= 64 points are taken whole: ~40 % fewer node visits for ~25 % more
+        // candidates (cfg1 count r = 3: 6.13 -> 5.04 ms, fill 5.22 -> 5.56 ms; LO_COARSE overrides)
+        static const u32 coarse = [] {
+            const char* e = std::getenv("LO_COARSE");
+            return e ? static_cast<u32>(std::strtoul(e, nullptr, 10)) : 64u;
+        }();
+        ft.coarse = coarse;
         const float compact = static_cast<float>(4.0 * r);
         u64* counter = dalloc_t<u64>(ctx, 1);
         LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));

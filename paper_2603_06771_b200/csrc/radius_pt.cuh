@@ -533,7 +533,8 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
                                         out_tile, mine, mymask);
             if (!FILL) {
                 mine += __popc(mymask);
-                if (rec_tile) {
+                // buffers without members leave no record (the replay would skip them anyway)
+                if (rec_tile && __any_sync(~0u, mymask != 0)) {
                     if (nrec < rp.cap) {
                         u32* R = rec_tile + nrec * 64;
                         R[lane] = __float_as_uint(P.w);
@@ -549,7 +550,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
         while (sp > 0) {
             const u32 t = S.stack[--sp];
             const NodeF nd = load_node_f(tf, t);
-            if (nd.nchild != 0) {
+            if (nd.nchild != 0 && nd.end - nd.begin > ft.coarse) {
                 bool keep = false;
                 if (cl < static_cast<int>(nd.nchild)) {
                     const NodeF ch = load_node_f(tf, nd.child0 + cl);

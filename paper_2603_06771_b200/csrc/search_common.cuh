@@ -143,6 +143,7 @@ struct FloatTest {
     float t_lo, t_hi;  // squared-distance thresholds (Sphere, Circle)
     float r_lo, r_hi;  // L-inf thresholds (Cube, Square)
     int enabled;
+    u32 coarse = 0;  // radius walk: internal nodes with at most this many points are taken whole
 };
 
 inline FloatTest make_float_test(double r, double bmax) {
