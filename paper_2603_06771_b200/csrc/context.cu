@@ -513,6 +513,7 @@ int lo_context_synchronize(lo_context* ctx) {
         LO_CUDA(cudaStreamSynchronize(ctx->h2d_stream));
         LO_CUDA(cudaStreamSynchronize(ctx->aux_stream));
         reclaim(ctx, true);
+        cache_drain(ctx);  // parked result buffers go back to the pool (bounded between syncs)
     });
 }
 void* lo_context_stream(lo_context* ctx) { return ctx ? ctx->stream : nullptr; }

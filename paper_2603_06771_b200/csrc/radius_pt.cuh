@@ -234,7 +234,7 @@ static __global__ void __launch_bounds__(128) radius_replay_bm_kernel(
 // buffer b; a warp scan of the popcounts gives every buffer's CSR start, and the write loop is two
 // shuffles, one shared load and one coalesced store per (row, buffer with members).
 constexpr u32 kReplayMaskStride = 33;
-constexpr size_t kReplayWarpWords = 32 * 32 + 32 * kReplayMaskStride;
+constexpr size_t kReplayWarpWords = 32 * 32 + 32 * kReplayMaskStride + 2 * 32 * 2;
 constexpr size_t kReplaySmem = kReplayWarps * kReplayWarpWords * 4;
 
 static __global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_kernel(
@@ -246,6 +246,12 @@ static __global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_ker
     const u32 lt = (1u << lane) - 1u;
     u32* I = replay_smem + w * kReplayWarpWords;  // [32][32] slot indices
     u32* M = I + 32 * 32;                         // [32][33] per-row masks
+    // per buffer (mask, CSR start) of the two rows in flight: the write loop reads them with one
+    // broadcast 8-byte shared load instead of two shuffles (the MIO pipe is the step's limit)
+    uint2* RM1 = reinterpret_cast<uint2*>(M + 32 * kReplayMaskStride);
+    uint2* RM2 = RM1 + 32;
+    const u32 rm1 = static_cast<u32>(__cvta_generic_to_shared(RM1));
+    const u32 rm2 = static_cast<u32>(__cvta_generic_to_shared(RM2));
     const u32 ih = static_cast<u32>(__cvta_generic_to_shared(I + lane));
     const u64 ntiles = (m + 31) / 32;
     for (u64 tile = static_cast<u64>(blockIdx.x) * kReplayWarps + w; tile < ntiles;
@@ -315,21 +321,24 @@ static __global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_ker
                 if (lane == L1) adv = tot1;
                 if (two && lane == L2) adv = tot2;
                 unsigned nz1 = __ballot_sync(~0u, m1 != 0), nz2 = __ballot_sync(~0u, m2 != 0);
-                auto step = [&](unsigned& nz, u32 mk, u32 pk) {
-                    const int b = __ffs(nz) - 1;
-                    nz &= nz - 1;
-                    const u32 mL = __shfl_sync(~0u, mk, b);
-                    const u32 pL = __shfl_sync(~0u, pk, b);
-                    u32 idx;
+                __syncwarp();  // the previous pair's write loop is done with RM1 / RM2
+                RM1[lane] = make_uint2(m1, p1);
+                RM2[lane] = make_uint2(m2, p2);
+                __syncwarp();
+                auto step = [&](unsigned& nz, u32 rm) {
+                    const int b = 31 - __clz(nz);  // order is free: every buffer's start is known
+                    nz ^= 1u << b;
+                    u32 mL, pL, idx;
+                    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mL), "=r"(pL) : "r"(rm + b * 8) : "memory");
                     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(idx) : "r"(ih + b * 128) : "memory");
                     if ((mL >> lane) & 1u) __stcg(out_tile + (pL + __popc(mL & lt)), idx);
                 };
                 while (nz1 && nz2) {
-                    step(nz1, m1, p1);
-                    step(nz2, m2, p2);
+                    step(nz1, rm1);
+                    step(nz2, rm2);
                 }
-                while (nz1) step(nz1, m1, p1);
-                while (nz2) step(nz2, m2, p2);
+                while (nz1) step(nz1, rm1);
+                while (nz2) step(nz2, rm2);
             }
             cursor += adv;
         }
