@@ -248,10 +248,8 @@ static __global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_ker
     u32* M = I + 32 * 32;                         // [32][33] per-row masks
     // per buffer (mask, CSR start) of the two rows in flight: the write loop reads them with one
     // broadcast 8-byte shared load instead of two shuffles (the MIO pipe is the step's limit)
-    uint2* RM1 = reinterpret_cast<uint2*>(M + 32 * kReplayMaskStride);
-    uint2* RM2 = RM1 + 32;
-    const u32 rm1 = static_cast<u32>(__cvta_generic_to_shared(RM1));
-    const u32 rm2 = static_cast<u32>(__cvta_generic_to_shared(RM2));
+    uint4* RM = reinterpret_cast<uint4*>(M + 32 * kReplayMaskStride);  // [b] = (m1, p1, m2, p2)
+    const u32 rmh = static_cast<u32>(__cvta_generic_to_shared(RM));
     const u32 ih = static_cast<u32>(__cvta_generic_to_shared(I + lane));
     const u64 ntiles = (m + 31) / 32;
     for (u64 tile = static_cast<u64>(blockIdx.x) * kReplayWarps + w; tile < ntiles;
@@ -321,24 +319,34 @@ static __global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_ker
                 if (lane == L1) adv = tot1;
                 if (two && lane == L2) adv = tot2;
                 unsigned nz1 = __ballot_sync(~0u, m1 != 0), nz2 = __ballot_sync(~0u, m2 != 0);
-                __syncwarp();  // the previous pair's write loop is done with RM1 / RM2
-                RM1[lane] = make_uint2(m1, p1);
-                RM2[lane] = make_uint2(m2, p2);
+                __syncwarp();  // the previous pair's write loop is done with RM
+                RM[lane] = make_uint4(m1, p1, m2, p2);
                 __syncwarp();
-                auto step = [&](unsigned& nz, u32 rm) {
-                    const int b = 31 - __clz(nz);  // order is free: every buffer's start is known
-                    nz ^= 1u << b;
-                    u32 mL, pL, idx;
-                    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(mL), "=r"(pL) : "r"(rm + b * 8) : "memory");
+                // one pass over the union of both rows' buffers: a buffer both rows draw from
+                // (the common case for neighbouring queries) costs one index load for the two stores
+                auto step = [&](int b) {
+                    u32 mA, pA, mB, pB, idx;
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(mA), "=r"(pA), "=r"(mB), "=r"(pB)
+                                 : "r"(rmh + b * 16)
+                                 : "memory");
                     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(idx) : "r"(ih + b * 128) : "memory");
-                    if ((mL >> lane) & 1u) __stcg(out_tile + (pL + __popc(mL & lt)), idx);
+                    if ((mA >> lane) & 1u) __stcg(out_tile + (pA + __popc(mA & lt)), idx);
+                    if ((mB >> lane) & 1u) __stcg(out_tile + (pB + __popc(mB & lt)), idx);
                 };
-                while (nz1 && nz2) {
-                    step(nz1, rm1);
-                    step(nz2, rm2);
+                unsigned nz = nz1 | nz2;
+                while (nz) {
+                    const int b1 = 31 - __clz(nz);  // order is free: every buffer's start is known
+                    nz ^= 1u << b1;
+                    if (nz) {
+                        const int b2 = 31 - __clz(nz);
+                        nz ^= 1u << b2;
+                        step(b1);
+                        step(b2);
+                    } else {
+                        step(b1);
+                    }
                 }
-                while (nz1) step(nz1, rm1);
-                while (nz2) step(nz2, rm2);
             }
             cursor += adv;
         }
