@@ -11,8 +11,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "liblinoct_b200.so")
+# LO_BUILD_DIR / LO_NVCC_EXTRA: side builds of tuning variants (objects + library elsewhere)
+OBJ = os.path.join(os.environ.get("LO_BUILD_DIR", HERE), "_build")
+LIB = os.path.join(os.environ.get("LO_BUILD_DIR", HERE), "liblinoct_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CUDA_SOURCES = ["context.cu", "reorder.cu", "octree.cu", "radius.cu", "radius_struct.cu", "knn.cu", "io.cu", "centres.cu"]
@@ -24,7 +25,7 @@ NVCC_FLAGS = [
     "-std=c++20", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
     "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "--expt-relaxed-constexpr",
     "-Xptxas", "-warn-spills",
-]
+] + os.environ.get("LO_NVCC_EXTRA", "").split()
 
 
 def _stale(src: str, obj: str, deps: list[str]) -> bool:

@@ -234,10 +234,18 @@ static __global__ void __launch_bounds__(128) radius_replay_bm_kernel(
 // buffer b; a warp scan of the popcounts gives every buffer's CSR start, and the write loop is two
 // shuffles, one shared load and one coalesced store per (row, buffer with members).
 constexpr u32 kReplayMaskStride = 33;
-constexpr size_t kReplayWarpWords = 32 * 32 + 32 * kReplayMaskStride + 2 * 32 * 2;
+#ifndef LO_REPLAY_ROWS
+#define LO_REPLAY_ROWS 4
+#endif
+#ifndef LO_REPLAY_BLOCKS
+#define LO_REPLAY_BLOCKS 5
+#endif
+constexpr int kReplayRows = LO_REPLAY_ROWS;  // rows per write pass (even)
+constexpr int kReplayBlocks = LO_REPLAY_BLOCKS;
+constexpr size_t kReplayWarpWords = 32 * 32 + 32 * kReplayMaskStride + 32 * 2 * kReplayRows;
 constexpr size_t kReplaySmem = kReplayWarps * kReplayWarpWords * 4;
 
-static __global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_kernel(
+static __global__ void __launch_bounds__(32 * kReplayWarps, kReplayBlocks) radius_replay_kernel(
     RecPool rp, u64 m, const u64* __restrict__ offsets, u32* __restrict__ out,
     u32* __restrict__ overflow_list, u32* __restrict__ overflow_n) {
     extern __shared__ __align__(16) u32 replay_smem[];
@@ -248,7 +256,7 @@ static __global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_ker
     u32* M = I + 32 * 32;                         // [32][33] per-row masks
     // per buffer (mask, CSR start) of the two rows in flight: the write loop reads them with one
     // broadcast 8-byte shared load instead of two shuffles (the MIO pipe is the step's limit)
-    uint4* RM = reinterpret_cast<uint4*>(M + 32 * kReplayMaskStride);  // [b] = (m1, p1, m2, p2)
+    uint4* RM = reinterpret_cast<uint4*>(M + 32 * kReplayMaskStride);  // [b][r/2] = (m, p) of rows r, r+1
     const u32 rmh = static_cast<u32>(__cvta_generic_to_shared(RM));
     const u32 ih = static_cast<u32>(__cvta_generic_to_shared(I + lane));
     const u64 ntiles = (m + 31) / 32;
@@ -294,47 +302,59 @@ static __global__ void __launch_bounds__(32 * kReplayWarps, 6) radius_replay_ker
                 }
             }
             __syncwarp();
-            // rows two at a time: the two rows' scans and write loops are independent chains
+            // kReplayRows rows per pass: their scans are independent chains, and the write loop runs
+            // once over the union of their buffers -- neighbouring queries draw on mostly the same
+            // buffers, so one index load serves up to kReplayRows stores
             unsigned rows = rows_all;
             u32 adv = 0;  // lane L: row L's members in this half
+            const bool in = static_cast<u32>(lane) < nh;
             while (rows) {
-                const int L1 = __ffs(rows) - 1;
-                rows &= rows - 1;
-                const int L2 = rows ? __ffs(rows) - 1 : L1;
-                const bool two = rows != 0;
-                rows &= rows - 1;
-                const bool in = static_cast<u32>(lane) < nh;
-                const u32 m1 = in ? M[lane * kReplayMaskStride + L1] : 0u;
-                const u32 m2 = in && two ? M[lane * kReplayMaskStride + L2] : 0u;
-                const u32 a1 = __popc(m1), a2 = __popc(m2);
-                u32 s1 = a1, s2 = a2;  // inclusive scans
+                int Ls[kReplayRows];
+                u32 mk[kReplayRows], sc[kReplayRows], pk[kReplayRows];
+                bool val[kReplayRows];
+                u32 any = 0;
+#pragma unroll
+                for (int r = 0; r < kReplayRows; ++r) {
+                    val[r] = rows != 0;
+                    Ls[r] = val[r] ? __ffs(rows) - 1 : 0;
+                    rows &= rows - 1;
+                    mk[r] = in && val[r] ? M[lane * kReplayMaskStride + Ls[r]] : 0u;
+                    sc[r] = __popc(mk[r]);
+                    any |= mk[r];
+                }
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
-                    const u32 t1 = __shfl_up_sync(~0u, s1, o), t2 = __shfl_up_sync(~0u, s2, o);
-                    if (lane >= o) s1 += t1, s2 += t2;
+#pragma unroll
+                    for (int r = 0; r < kReplayRows; ++r) {
+                        const u32 t = __shfl_up_sync(~0u, sc[r], o);
+                        if (lane >= o) sc[r] += t;
+                    }
                 }
-                const u32 p1 = __shfl_sync(~0u, cursor, L1) + s1 - a1;  // exclusive starts
-                const u32 p2 = __shfl_sync(~0u, cursor, L2) + s2 - a2;
-                const u32 tot1 = __shfl_sync(~0u, s1, 31), tot2 = __shfl_sync(~0u, s2, 31);
-                if (lane == L1) adv = tot1;
-                if (two && lane == L2) adv = tot2;
-                unsigned nz1 = __ballot_sync(~0u, m1 != 0), nz2 = __ballot_sync(~0u, m2 != 0);
-                __syncwarp();  // the previous pair's write loop is done with RM
-                RM[lane] = make_uint4(m1, p1, m2, p2);
+#pragma unroll
+                for (int r = 0; r < kReplayRows; ++r) {
+                    pk[r] = __shfl_sync(~0u, cursor, Ls[r]) + sc[r] - __popc(mk[r]);  // exclusive starts
+                    const u32 tot = __shfl_sync(~0u, sc[r], 31);
+                    if (val[r] && lane == Ls[r]) adv = tot;
+                }
+                unsigned nz = __ballot_sync(~0u, any != 0);
+                __syncwarp();  // the previous pass's write loop is done with RM
+#pragma unroll
+                for (int r = 0; r < kReplayRows; r += 2) RM[lane * (kReplayRows / 2) + r / 2] = make_uint4(mk[r], pk[r], mk[r + 1], pk[r + 1]);
                 __syncwarp();
-                // one pass over the union of both rows' buffers: a buffer both rows draw from
-                // (the common case for neighbouring queries) costs one index load for the two stores
                 auto step = [&](int b) {
-                    u32 mA, pA, mB, pB, idx;
-                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(mA), "=r"(pA), "=r"(mB), "=r"(pB)
-                                 : "r"(rmh + b * 16)
-                                 : "memory");
+                    u32 idx;
                     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(idx) : "r"(ih + b * 128) : "memory");
-                    if ((mA >> lane) & 1u) __stcg(out_tile + (pA + __popc(mA & lt)), idx);
-                    if ((mB >> lane) & 1u) __stcg(out_tile + (pB + __popc(mB & lt)), idx);
+#pragma unroll
+                    for (int r = 0; r < kReplayRows; r += 2) {
+                        u32 mA, pA, mB, pB;
+                        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(mA), "=r"(pA), "=r"(mB), "=r"(pB)
+                                     : "r"(rmh + (b * (kReplayRows / 2) + r / 2) * 16)
+                                     : "memory");
+                        if ((mA >> lane) & 1u) __stcg(out_tile + (pA + __popc(mA & lt)), idx);
+                        if ((mB >> lane) & 1u) __stcg(out_tile + (pB + __popc(mB & lt)), idx);
+                    }
                 };
-                unsigned nz = nz1 | nz2;
                 while (nz) {
                     const int b1 = 31 - __clz(nz);  // order is free: every buffer's start is known
                     nz ^= 1u << b1;
@@ -440,10 +460,11 @@ static inline u32 replay_records(lo_context* ctx, const RecSetup& rs, u64 m, con
     const u64 tiles = (m + 31) / 32;
     LO_CUDA(cudaMemsetAsync(rs.ovf_n, 0, 4, ctx->stream));
     // short rows: buffer-major stores stay line-local; long rows: row-major so every output line
-    // completes while hot (measured crossover ~ 64-96 members per row on cfg0 / cfg1 / cfg4)
+    // completes while hot (measured crossover ~ 32-45 members per row: cfg1 r = 1 (31.5) is faster
+    // buffer-major, cfg4 (45) and cfg0 (65) row-major)
     static const u64 row_major_min = [] {
         const char* e = std::getenv("LO_REPLAY_ROW_MAJOR_MIN");
-        return e ? std::strtoull(e, nullptr, 10) : 96ull;
+        return e ? std::strtoull(e, nullptr, 10) : 40ull;
     }();
     if (total < row_major_min * m) {
         const int rb = static_cast<int>(std::max<u64>(
@@ -457,7 +478,7 @@ static inline u32 replay_records(lo_context* ctx, const RecSetup& rs, u64 m, con
         }();
         (void)attr;
         const int rr = static_cast<int>(std::max<u64>(
-            1, std::min<u64>((tiles + kReplayWarps - 1) / kReplayWarps, ctx->sm_count * 6ull)));
+            1, std::min<u64>((tiles + kReplayWarps - 1) / kReplayWarps, ctx->sm_count * static_cast<u64>(kReplayBlocks))));
         radius_replay_kernel<<<rr, 32 * kReplayWarps, kReplaySmem, ctx->stream>>>(rs.rp, m, offsets, out, rs.ovf,
                                                                                 rs.ovf_n);
     }
