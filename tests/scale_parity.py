@@ -1,7 +1,8 @@
 """Full-size parity of the B200 path against the reference library (oracle/_ref) on every
 BASELINE config (cfg0..cfg4).  Run on a GPU box:
 
-    python tests/scale_parity.py [--configs cfg0 cfg1 ...] [--centres 20000] > profiles/r1/scale_parity.txt
+    python tests/scale_parity.py [--configs cfg0 cfg1 ...] [--centres 20000] [--full cfg0 cfg1 ...] \
+        > profiles/r1/scale_parity.txt
 
 For each config the whole structure is compared bit for bit (sorted codes, permutation,
 reordered coordinates, LeafArray, InternalNode table); radius counts and FNV-1a digests are
@@ -27,7 +28,7 @@ from oracle.oracle_py import Ref  # noqa: E402
 from paper_2603_06771_b200 import linoct as lo  # noqa: E402
 
 
-def check(cfg_name: str, centres: int) -> list[str]:
+def check(cfg_name: str, centres: int, full_cfgs=("cfg0",)) -> list[str]:
     cfg = bench.CONFIGS[cfg_name]
     out = []
     t0 = time.time()
@@ -49,7 +50,7 @@ def check(cfg_name: str, centres: int) -> list[str]:
     out.append(f"{cfg_name}: leaves={len(b) - 1} internal={len(nodes)} LeafArray + InternalNode table "
                f"bit-exact: {ok_t}")
     del b, o, nodes
-    full = cfg_name == "cfg0"
+    full = cfg_name in full_cfgs
     for r in cfg["radii"]:
         if full:
             want = p.radius(r, method=1)
@@ -65,10 +66,15 @@ def check(cfg_name: str, centres: int) -> list[str]:
         out.append(f"{cfg_name}: radius r={r} on {len(got.centers)} centres: counts + FNV digests equal: "
                    f"{okr} (mu={got.counts.mean():.2f})")
     for k in cfg["ks"]:
-        m = max(1000, centres // 4)
-        want = p.knn(k, mode=1, subset=m, seed=77 + k)
-        got = lo.run_knn_batch(tree, coded, k, lo.BatchOptions(mode=lo.BatchMode.RandomSubset,
-                                                               subset_size=m, seed=77 + k))
+        if full:
+            want = p.knn(k)
+            got = lo.run_knn_batch(tree, coded, k, lo.BatchOptions())
+            m = len(got.centers)
+        else:
+            m = max(1000, centres // 4)
+            want = p.knn(k, mode=1, subset=m, seed=77 + k)
+            got = lo.run_knn_batch(tree, coded, k, lo.BatchOptions(mode=lo.BatchMode.RandomSubset,
+                                                                   subset_size=m, seed=77 + k))
         okk = np.array_equal(got.centers, want["centers"]) and np.array_equal(got.fingerprints, want["fps"])
         out.append(f"{cfg_name}: kNN k={k} on {m} centres: (index, dist_sq) FNV digests equal: {okk}")
     out.append(f"{cfg_name}: reference build {t_ref:.1f}s, total {time.time() - t0:.1f}s")
@@ -79,10 +85,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", nargs="*", default=["cfg0", "cfg1", "cfg4", "cfg3"])
     ap.add_argument("--centres", type=int, default=20000)
+    ap.add_argument("--full", nargs="*", default=["cfg0"],
+                    help="configs compared on every point as a centre (Full mode) instead of a subset")
     a = ap.parse_args()
     allok = True
     for c in a.configs:
-        for line in check(c, a.centres):
+        for line in check(c, a.centres, tuple(a.full)):
             print(line, flush=True)
             allok &= ": False" not in line
     print("ALL EQUAL" if allok else "MISMATCH")
