@@ -186,7 +186,7 @@ __device__ __forceinline__ void knn_offer(Heap& heap, u32 k, Key& worst_k, u32& 
 
 // Tests the `cnt` staged candidates against this lane's query (pairs, packed FP32).
 template <int KC, class Heap, class Key>
-__device__ __forceinline__ void knn_chunk(const KnnSmem& S, u32 cnt, bool active, u64 QX, u64 QY,
+__device__ __forceinline__ void knn_chunk_each(const KnnSmem& S, u32 cnt, bool active, u64 QX, u64 QY,
                                           u64 QZ, Heap& heap, u32 k, Key& worst_d,
                                           u32& worst_i, float& T, float E, double cx, double cy,
                                           double cz, u32 skip_lo, u32 skip_hi) {
@@ -214,6 +214,66 @@ __device__ __forceinline__ void knn_chunk(const KnnSmem& S, u32 cnt, bool active
                 knn_offer<KC>(heap, k, worst_d, worst_i, T, E, v1, g, cx, cy, cz, S.pd + 6 * pp + 3);
         }
     }
+}
+
+// Tests the `cnt` staged candidates against this lane's query (pairs, packed FP32).  First every
+// lane marks the candidates under its current threshold T, then the lanes offer their marked
+// candidates in lockstep (ascending slot order, as before): once the heaps are full the passes are
+// sparse and spread over the lanes, and offering candidate by candidate ran a warp-wide heap sift
+// for every candidate any single lane wanted.  T only tightens, so re-checking a mark against the
+// current T (knn_offer) keeps the result identical.  Measured faster for k = 8 only (6.98 vs 7.27 ms
+// at cfg1); for k >= 16 the extra registers spill and it lost 3-7 %.
+template <int KC, class Heap, class Key>
+__device__ __forceinline__ void knn_chunk_marked(const KnnSmem& S, u32 cnt, bool active, u64 QX, u64 QY,
+                                          u64 QZ, Heap& heap, u32 k, Key& worst_d,
+                                          u32& worst_i, float& T, float E, double cx, double cy,
+                                          double cz, u32 skip_lo, u32 skip_hi) {
+    if (!active) return;
+    const u32 npairs = (cnt + 1) >> 1;
+    u32 pass = 0;
+    for (u32 pp = 0; pp < npairs; ++pp) {
+        const float4 a = S.pa[pp];
+        const float2 b = S.pb[pp];
+        const u64 dx = fsub2(pack2(a.x, a.y), QX);
+        const u64 dy = fsub2(pack2(a.z, a.w), QY);
+        const u64 dz = fsub2(pack2(b.x, b.y), QZ);
+        u64 d2 = fmul2(dx, dx);
+        d2 = ffma2(dy, dy, d2);
+        d2 = ffma2(dz, dz, d2);
+        float v0, v1;
+        unpack2(d2, v0, v1);
+        pass |= (v0 <= T ? 1u : 0u) << (2 * pp);
+        pass |= (v1 <= T ? 1u : 0u) << (2 * pp + 1);
+    }
+    if (cnt < 32) pass &= (1u << cnt) - 1u;
+    const float qx = __uint_as_float(static_cast<u32>(QX)), qy = __uint_as_float(static_cast<u32>(QY)),
+                qz = __uint_as_float(static_cast<u32>(QZ));
+    while (pass) {
+        const int j = __ffs(pass) - 1;
+        pass &= pass - 1;
+        const u32 g = S.pidx[j];
+        if (g >= skip_lo && g < skip_hi) continue;
+        // the same FP32 expression as the packed one above (FADD2/FMUL2/FFMA2 are per-lane IEEE ops)
+        const float* a = reinterpret_cast<const float*>(S.pa);
+        const float* bb = reinterpret_cast<const float*>(S.pb);
+        const int pp = j >> 1, h = j & 1;
+        const float dx = a[4 * pp + h] - qx, dy = a[4 * pp + 2 + h] - qy, dz = bb[2 * pp + h] - qz;
+        const float v = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+        knn_offer<KC>(heap, k, worst_d, worst_i, T, E, v, g, cx, cy, cz, S.pd + 3 * j);
+    }
+}
+
+template <int KC, class Heap, class Key>
+__device__ __forceinline__ void knn_chunk(const KnnSmem& S, u32 cnt, bool active, u64 QX, u64 QY,
+                                          u64 QZ, Heap& heap, u32 k, Key& worst_d,
+                                          u32& worst_i, float& T, float E, double cx, double cy,
+                                          double cz, u32 skip_lo, u32 skip_hi) {
+    if constexpr (KC == 8)
+        knn_chunk_marked<KC>(S, cnt, active, QX, QY, QZ, heap, k, worst_d, worst_i, T, E, cx, cy, cz, skip_lo,
+                             skip_hi);
+    else
+        knn_chunk_each<KC>(S, cnt, active, QX, QY, QZ, heap, k, worst_d, worst_i, T, E, cx, cy, cz, skip_lo,
+                           skip_hi);
 }
 
 // Stage points [base, base + cnt) (cnt <= 32) of the sorted cloud: FP32 pairs for the filter,
