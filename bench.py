@@ -205,7 +205,10 @@ def config_block(args, cfg):
     return {"workload": args.config, "points": cfg["n"], "cloud": cfg["kind"],
             "curve": "hilbert" if cfg["curve"] else "morton", "leaf_bucket": cfg["n_max"],
             "radii": cfg["radii"], "knn_k": cfg["ks"], "queries_per_step": len(cfg["radii"]) * cfg["n"],
-            "parallelism": f"query-shard x{args.gpus} (structure broadcast)" if args.gpus > 1 else "1 GPU",
+            "parallelism": (f"query-shard x{args.gpus} (" + ("structure broadcast from rank 0"
+                                                            if os.environ.get("LO_BENCH_BROADCAST") == "1"
+                                                            else "structure built on every rank") + ")")
+            if args.gpus > 1 else "1 GPU",
             "l2": "inputs larger than L2 (cloud 24 B/pt + multi-GB CSR per step)"}
 
 
@@ -239,9 +242,14 @@ def run_ours(args, cfg):
     n = cfg["n"]
     radii = cfg["radii"]
 
-    xyz_host = generate(cfg) if rank == 0 else None
+    # N > 1: every rank builds the (deterministic, bit-identical) structure from its own copy of the
+    # cloud -- 2.4 ms of reorder + build per step instead of the same on rank 0 plus a ~600 MB
+    # broadcast (SURVEY.md §8e step 1's alternative); LO_BENCH_BROADCAST=1 broadcasts from rank 0
+    replicate = world > 1 and os.environ.get("LO_BENCH_BROADCAST") != "1"
+    builds = rank == 0 or replicate
+    xyz_host = generate(cfg) if builds else None
     xyz_dev = C.c_void_p()
-    if rank == 0:
+    if builds:
         _lib.check(L.lo_device_alloc(ctx.h, 24 * n, C.byref(xyz_dev)))
         _lib.check(L.lo_memcpy_h2d(ctx.h, xyz_dev, xyz_host.ctypes.data, 24 * n))
 
@@ -251,12 +259,12 @@ def run_ours(args, cfg):
 
     def build_structure():
         coded = tree = None
-        if rank == 0:
+        if builds:
             coded = C.c_void_p()
             _lib.check(L.lo_reorder_device(ctx.h, xyz_dev, n, cfg["curve"], 21, C.byref(coded)))
             tree = C.c_void_p()
             _lib.check(L.lo_octree_build(ctx.h, coded, cfg["n_max"], C.byref(tree)))
-        if world > 1:
+        if world > 1 and not replicate:
             coded, tree, _, _ = D.broadcast_structure(ctx, coded, tree, src=0)
         return coded, tree
 
@@ -363,7 +371,7 @@ def run_ours(args, cfg):
     e2e = None
     if not args.no_e2e:
         pinned = C.c_void_p()
-        if rank == 0:
+        if builds:
             _lib.check(L.lo_host_alloc_pinned(24 * n, C.byref(pinned)))
             C.memmove(pinned, xyz_host.ctypes.data, 24 * n)
         rows = b1 - b0
@@ -381,17 +389,17 @@ def run_ours(args, cfg):
         # input pipeline: step s+1's cloud uploads (lo_h2d_begin, its own stream) while step s
         # computes; every step still moves its 24 B/pt in and its counts + digests out
         dev_in = [C.c_void_p(), C.c_void_p()]
-        if rank == 0:
+        if builds:
             for d in dev_in:
                 _lib.check(L.lo_device_alloc(ctx.h, 24 * n, C.byref(d)))
 
         def e2e_run(steps):
-            if rank == 0:
+            if builds:
                 _lib.check(L.lo_h2d_begin(ctx.h, dev_in[0], pinned, 24 * n, 0))
             for s in range(steps):
                 cur = s % 2
                 coded = tree = None
-                if rank == 0:
+                if builds:
                     if s + 1 < steps:
                         _lib.check(L.lo_h2d_begin(ctx.h, dev_in[1 - cur], pinned, 24 * n, 1 - cur))
                     _lib.check(L.lo_h2d_wait(ctx.h, cur))
@@ -399,7 +407,7 @@ def run_ours(args, cfg):
                     _lib.check(L.lo_reorder_device(ctx.h, dev_in[cur], n, cfg["curve"], 21, C.byref(coded)))
                     tree = C.c_void_p()
                     _lib.check(L.lo_octree_build(ctx.h, coded, cfg["n_max"], C.byref(tree)))
-                if world > 1:
+                if world > 1 and not replicate:
                     coded, tree, _, _ = D.broadcast_structure(ctx, coded, tree, src=0)
                 if s >= 2:
                     _lib.check(L.lo_d2h_wait(ctx.h, cur))  # step s - 2's results are on the host
@@ -430,12 +438,12 @@ def run_ours(args, cfg):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": len(radii) * n / (ems * 1e-3), "unit": "queries/s", "ms_per_step": ems,
-               "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": len(radii) * 12 * n,
+               "h2d_bytes_per_step": 24 * n * (world if replicate else 1), "d2h_bytes_per_step": len(radii) * 12 * n,
                "path": "lo_h2d_begin(pinned cloud, next step's upload overlapped) -> lo_reorder_device -> "
                        "lo_octree_build -> lo_radius_range(+FNV) -> lo_csr_download_async(counts, digests; "
                        "overlapped with the next radius and step; host buffers double-buffered behind "
                        "lo_d2h_fence/lo_d2h_wait) -> lo_context_synchronize"}
-        if rank == 0:
+        if builds:
             L.lo_host_free_pinned(pinned)
             for d in dev_in:
                 L.lo_device_free(ctx.h, d)
