@@ -7,6 +7,7 @@
 // indices of the SFC-sorted cloud, so sorting them by value IS sorting them along the curve:
 // one stable radix sort (payload = position), search, then scatter rows / counts / digests back
 // to the caller's order.
+#include <cstring>
 #include <algorithm>
 #include <vector>
 
@@ -61,8 +62,8 @@ SortedCentres sort_centres(lo_context* ctx, const u32* centres, u64 m) {
         digit_hist_u32<<<std::min(grid_n(ctx, m), ctx->sm_count * 2), 256, 0, ctx->stream>>>(centres, m, hist);
         LO_CHECK_LAUNCH();
         std::vector<u32> hh(8 * 256, 0);
-        LO_CUDA(cudaMemcpyAsync(hh.data(), hist, 4 * 256 * 4, cudaMemcpyDeviceToHost, ctx->stream));
-        sync(ctx);
+        fetch_small(ctx, hist, 4 * 256 * 4);
+        std::memcpy(hh.data(), ctx->pinned_scratch, 4 * 256 * 4);
         hh[4 * 256] = static_cast<u32>(m);  // digit 4 (bits 32..39) is constant
         radix_sort(ctx, k64, m, hh.data(), 11, ks, s.pos);  // 11 levels = 33 bits -> 5 passes
         narrow_u64<<<grid_n(ctx, m), 256, 0, ctx->stream>>>(ks, m, s.idx);

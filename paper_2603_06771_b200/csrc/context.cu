@@ -148,6 +148,18 @@ void dfree(lo_context* ctx, void* p) {
 
 void sync(lo_context* ctx) { LO_CUDA(cudaStreamSynchronize(ctx->stream)); }
 
+__global__ void fetch_words(const u32* __restrict__ src, u32* dst, u32 words) {
+    for (u32 i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+}
+
+void fetch_small(lo_context* ctx, const void* dev, size_t bytes) {
+    require(bytes <= 16384 && bytes % 4 == 0, LO_INVALID_ARGUMENT, "fetch_small size");
+    fetch_words<<<1, 256, 0, ctx->stream>>>(static_cast<const u32*>(dev), static_cast<u32*>(ctx->pinned_scratch_dev),
+                                          static_cast<u32>(bytes / 4));
+    LO_CHECK_LAUNCH();
+    sync(ctx);
+}
+
 void* arena(lo_context* ctx, size_t bytes) {
     if (ctx->arena_bytes >= bytes) return ctx->arena;
     if (ctx->arena) {
@@ -470,7 +482,8 @@ int lo_context_create(int device, void* stream, lo_context** out) {
         LO_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
         u64 threshold = ~0ull;
         LO_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
-        LO_CUDA(cudaMallocHost(&ctx->pinned_scratch, 4096));
+        LO_CUDA(cudaHostAlloc(&ctx->pinned_scratch, 16384, cudaHostAllocMapped));
+        LO_CUDA(cudaHostGetDevicePointer(&ctx->pinned_scratch_dev, ctx->pinned_scratch, 0));
         curve_tables(LO_HILBERT);  // derive + self-check once
         *out = ctx;
     });

@@ -101,7 +101,8 @@ struct lo_context {
     };
     std::vector<Stage> stages;          // pending stage events (resolved on query)
     std::vector<std::pair<std::string, float>> stage_ms;
-    void* pinned_scratch = nullptr;     // small pinned buffer for scalar D2H
+    void* pinned_scratch = nullptr;     // small mapped pinned buffer for scalar reads
+    void* pinned_scratch_dev = nullptr; // its device alias
     void* arena = nullptr;              // persistent device scratch (radius records)
     size_t arena_bytes = 0;
     // asynchronous result downloads (lo_csr_download_async): D2H on a second stream so the
@@ -215,7 +216,10 @@ void unsort_csr(lo_context* ctx, const SortedCentres& s, lo_csr* c);
 void unsort_knn(lo_context* ctx, const SortedCentres& s, lo_knn_result* r);
 // reorder.cu: stable LSD sort of u64 keys (passes for `level`*3 bits, constant digits skipped
 // per hist_host[8*256]); perm = original positions.
-void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int level, u64* keys_sorted, u32* perm);
+// hist_dev (optional): the same histogram on the device -- the digit bases are then scanned there
+// instead of uploaded (no host->device copy that could queue behind a pending upload).
+void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int level, u64* keys_sorted, u32* perm,
+                const u32* hist_dev = nullptr);
 // reorder.cu: positions of arbitrary query points (SoA, device) in curve order.
 u32* sort_points_sfc(lo_context* ctx, const lo_coded* c, const double* x, const double* y, const double* z,
                      u64 m);
@@ -266,11 +270,14 @@ void* arena(lo_context* ctx, size_t bytes);
 void stage_begin(lo_context* ctx, const char* name);
 void stage_end(lo_context* ctx);
 void sync(lo_context* ctx);
+// Copies `bytes` (<= 16384, 4-byte aligned) of device memory into ctx->pinned_scratch and waits.
+// A one-warp kernel stores them through the mapped alias instead of a cudaMemcpy: a D2H copy on
+// the context stream queued behind the copy engine's pending result downloads (lo_csr_download_async
+// of the previous batch) and stalled every batch by the length of that download.
+void fetch_small(lo_context* ctx, const void* dev, size_t bytes);
 template <class T>
 T read_scalar(lo_context* ctx, const T* dev) {
-    LO_CUDA(cudaMemcpyAsync(ctx->pinned_scratch, dev, sizeof(T), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    sync(ctx);
+    fetch_small(ctx, dev, sizeof(T));
     T v;
     std::memcpy(&v, ctx->pinned_scratch, sizeof(T));
     return v;

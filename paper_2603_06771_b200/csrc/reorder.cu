@@ -1,6 +1,7 @@
 // reorder.cu -- K1 bbox, K2 encode (+ fused digit histograms), K3 onesweep LSD radix sort,
 // K4 SoA gather.  Replaces compute_codes / radix_sort_codes / reorder_cloud
 // (reorder.cpp:9-89) with bit-identical results (keys, stable permutation, coordinates).
+#include <cstring>
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
@@ -357,9 +358,8 @@ static Disc compute_disc(lo_context* ctx, const double* xyz_dev, u64 n, int leve
     bbox_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(xyz_dev, n, bb);
     LO_CHECK_LAUNCH();
     u64 h[7];
-    LO_CUDA(cudaMemcpyAsync(ctx->pinned_scratch, bb, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    fetch_small(ctx, bb, sizeof h);
     dfree(ctx, bb);
-    sync(ctx);
     std::memcpy(h, ctx->pinned_scratch, sizeof h);
     if (h[6] != ~0ull) {
         throw Error(LO_INVALID_ARGUMENT, "non-finite coordinate at point " + std::to_string(h[6]));
@@ -397,8 +397,19 @@ static EncodeParams make_params(const double box[6], const double scale[3], int 
 }
 
 // Sorts (codes, implicit original index) stably; writes sorted keys + perm.
+// Digit bases per pass: exclusive scan of each pass's 256 counts (thread = pass).
+__global__ void sort_bases(const u32* __restrict__ hist, u64* __restrict__ bases, int passes) {
+    const int p = threadIdx.x;
+    if (p >= passes) return;
+    u64 s = 0;
+    for (int b = 0; b < 256; ++b) {
+        bases[p * 256 + b] = s;
+        s += hist[p * 256 + b];
+    }
+}
+
 void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int level,
-                       u64* keys_sorted, u32* perm) {
+                       u64* keys_sorted, u32* perm, const u32* hist_dev) {
     const int passes = (3 * level + 7) / 8;
     // digit bases per pass and the constant-digit skip (reorder.cpp:49)
     std::vector<int> run;
@@ -422,8 +433,12 @@ void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int lev
     }
     const int tiles = ceil_div(n, kSortTile);
     u64* dbase = dalloc_t<u64>(ctx, 8 * 256);
-    LO_CUDA(cudaMemcpyAsync(dbase, bases.data(), bases.size() * 8, cudaMemcpyHostToDevice,
-                            ctx->stream));
+    if (hist_dev) {
+        sort_bases<<<1, 32, 0, ctx->stream>>>(hist_dev, dbase, passes);
+        LO_CHECK_LAUNCH();
+    } else {
+        LO_CUDA(cudaMemcpyAsync(dbase, bases.data(), bases.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
     u64* status = dalloc_t<u64>(ctx, static_cast<size_t>(tiles) * 256);
     u32* counter = dalloc_t<u32>(ctx, 1);
     u64* kalt = dalloc_t<u64>(ctx, n);
@@ -508,9 +523,9 @@ u32* sort_points_sfc(lo_context* ctx, const lo_coded* c, const double* x, const 
                                                                                               codes, hist);
         LO_CHECK_LAUNCH();
         std::vector<u32> hh(8 * 256);
-        LO_CUDA(cudaMemcpyAsync(hh.data(), hist, 8 * 256 * 4, cudaMemcpyDeviceToHost, ctx->stream));
-        sync(ctx);
-        radix_sort(ctx, codes, m, hh.data(), c->level, sorted, pos);
+        fetch_small(ctx, hist, 8 * 256 * 4);
+        std::memcpy(hh.data(), ctx->pinned_scratch, 8 * 256 * 4);
+        radix_sort(ctx, codes, m, hh.data(), c->level, sorted, pos, hist);
     } catch (...) {
         dfree(ctx, codes), dfree(ctx, sorted), dfree(ctx, hist), dfree(ctx, pos);
         throw;
@@ -548,14 +563,14 @@ lo_coded* reorder_device(lo_context* ctx, const double* xyz, u64 n, int curve, i
         LO_CHECK_LAUNCH();
         stage_end(ctx);
         std::vector<u32> hh(8 * 256 + 1);
-        LO_CUDA(cudaMemcpyAsync(hh.data(), hist, hh.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
-        sync(ctx);
+        fetch_small(ctx, hist, hh.size() * 4);
+        std::memcpy(hh.data(), ctx->pinned_scratch, hh.size() * 4);
         require(hh[8 * 256] == 0, LO_DOMAIN_ERROR, "point outside discretizer bounds");
 
         stage_begin(ctx, "sort");
         c->codes = dalloc_t<u64>(ctx, n);
         c->perm = dalloc_t<u32>(ctx, n);
-        radix_sort(ctx, codes, n, hh.data(), level, c->codes, c->perm);
+        radix_sort(ctx, codes, n, hh.data(), level, c->codes, c->perm, hist);
         stage_end(ctx);
         dfree(ctx, codes);
         dfree(ctx, hist);
