@@ -343,6 +343,19 @@ __device__ __forceinline__ u64 fnv_u32(u64 h, u32 v) {
     h *= P5;
     return h;
 }
+// The same for an index known to be < 2^24 (clouds of at most 16.7M points): its fourth byte is
+// zero as well, so five zero bytes fold into prime^6 (two fewer integer ops per index).
+__device__ __forceinline__ u64 fnv_u24(u64 h, u32 v) {
+    constexpr u64 P = 0x100000001b3ULL;
+    constexpr u64 P6 = P * P * P * P * P * P;
+    h ^= v & 0xffu;
+    h *= P;
+    h ^= (v >> 8) & 0xffu;
+    h *= P;
+    h ^= v >> 16;
+    h *= P6;
+    return h;
+}
 __device__ __forceinline__ u64 fnv_u64(u64 h, u64 v) {
     constexpr u64 P = 0x100000001b3ULL;
 #pragma unroll

@@ -89,35 +89,37 @@ __global__ void __launch_bounds__(kRadiusThreads) radius_kernel(
 // K8: FNV-1a-64 per row over its indices (search.cpp:345-347).  The hash chain is sequential
 // per row, so a thread owns a row; it reads the row with 16-byte loads (one L1 sector per load
 // instead of one per index) after peeling to 16-byte alignment.
+template <bool SMALL>
 __global__ void radius_digest(const u64* __restrict__ offsets, const u32* __restrict__ idx, u64 m,
                               u64* __restrict__ fps) {
     for (u64 r = blockIdx.x * (u64)blockDim.x + threadIdx.x; r < m;
          r += (u64)gridDim.x * blockDim.x) {
+        auto fnv = [](u64 h, u32 v) { return SMALL ? fnv_u24(h, v) : fnv_u32(h, v); };
         u64 h = kFnvOffset;
         u64 j = offsets[r];
         const u64 e = offsets[r + 1];
-        for (; j < e && (j & 3); ++j) h = fnv_u32(h, __ldg(idx + j));
+        for (; j < e && (j & 3); ++j) h = fnv(h, __ldg(idx + j));
         for (; j + 8 <= e; j += 8) {  // two loads in flight per iteration
             const uint4 v = __ldg(reinterpret_cast<const uint4*>(idx + j));
             const uint4 u = __ldg(reinterpret_cast<const uint4*>(idx + j + 4));
-            h = fnv_u32(h, v.x);
-            h = fnv_u32(h, v.y);
-            h = fnv_u32(h, v.z);
-            h = fnv_u32(h, v.w);
-            h = fnv_u32(h, u.x);
-            h = fnv_u32(h, u.y);
-            h = fnv_u32(h, u.z);
-            h = fnv_u32(h, u.w);
+            h = fnv(h, v.x);
+            h = fnv(h, v.y);
+            h = fnv(h, v.z);
+            h = fnv(h, v.w);
+            h = fnv(h, u.x);
+            h = fnv(h, u.y);
+            h = fnv(h, u.z);
+            h = fnv(h, u.w);
         }
         if (j + 4 <= e) {
             const uint4 v = __ldg(reinterpret_cast<const uint4*>(idx + j));
-            h = fnv_u32(h, v.x);
-            h = fnv_u32(h, v.y);
-            h = fnv_u32(h, v.z);
-            h = fnv_u32(h, v.w);
+            h = fnv(h, v.x);
+            h = fnv(h, v.y);
+            h = fnv(h, v.z);
+            h = fnv(h, v.w);
             j += 4;
         }
-        for (; j < e; ++j) h = fnv_u32(h, __ldg(idx + j));
+        for (; j < e; ++j) h = fnv(h, __ldg(idx + j));
         fps[r] = h;
     }
 }
@@ -267,15 +269,20 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
                 // readers of fps / indices (downloads, unsort, release) order behind `digested`
                 LO_CUDA(cudaStreamWaitEvent(ctx->aux_stream, e1, 0));
                 LO_CUDA(cudaEventCreateWithFlags(&out->digested, cudaEventDisableTiming));
-                radius_digest<<<std::max(1, ceil_div(q.m, 256)), 256, 0, ctx->aux_stream>>>(
-                    out->offsets, out->indices, q.m, out->fps);
+                if (c->n <= (1u << 24))
+                    radius_digest<true><<<std::max(1, ceil_div(q.m, 256)), 256, 0, ctx->aux_stream>>>(
+                        out->offsets, out->indices, q.m, out->fps);
+                else
+                    radius_digest<false><<<std::max(1, ceil_div(q.m, 256)), 256, 0, ctx->aux_stream>>>(
+                        out->offsets, out->indices, q.m, out->fps);
                 LO_CHECK_LAUNCH();
                 LO_CUDA(cudaEventRecord(out->digested, ctx->aux_stream));
             } else {
                 stage_begin(ctx, "radius_digest");
                 if (q.m)
-                    radius_digest<<<std::max(1, ceil_div(q.m, 256)), 256, 0, ctx->stream>>>(
-                        out->offsets, out->indices, q.m, out->fps);
+                    (c->n <= (1u << 24) ? radius_digest<true> : radius_digest<false>)
+                        <<<std::max(1, ceil_div(q.m, 256)), 256, 0, ctx->stream>>>(out->offsets, out->indices, q.m,
+                                                                                   out->fps);
                 LO_CHECK_LAUNCH();
                 stage_end(ctx);
                 LO_CUDA(cudaEventRecord(e1, ctx->stream));
