@@ -11,6 +11,10 @@
  *   LO_INVALID_ARGUMENT <-> std::invalid_argument, LO_DOMAIN_ERROR <-> std::domain_error,
  *   LO_LOGIC_ERROR <-> std::logic_error.  lo_last_error() returns the message of the last
  *   failure on the calling host thread.
+ *
+ * Threading (search.hpp:119-120): calls on one lo_context are serialized by the
+ * context's lock, so several host threads may share a context; built handles are read-only.
+ * lo_context_destroy must not race other calls on the same context.
  */
 #ifndef LINOCT_B200_H
 #define LINOCT_B200_H

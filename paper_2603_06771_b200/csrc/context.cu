@@ -520,7 +520,7 @@ int lo_context_destroy(lo_context* ctx) {
 }
 
 int lo_context_synchronize(lo_context* ctx) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         sync(ctx);
         LO_CUDA(cudaStreamSynchronize(ctx->copy_stream));
         LO_CUDA(cudaStreamSynchronize(ctx->h2d_stream));
@@ -532,7 +532,7 @@ int lo_context_synchronize(lo_context* ctx) {
 void* lo_context_stream(lo_context* ctx) { return ctx ? ctx->stream : nullptr; }
 
 int lo_context_set_timing(lo_context* ctx, int enabled) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         ctx->timing = enabled != 0;
         ctx->stage_ms.clear();
     });
@@ -540,7 +540,7 @@ int lo_context_set_timing(lo_context* ctx, int enabled) {
 
 int lo_context_stage_times(lo_context* ctx, char* names, int name_len, double* ms, int cap) {
     int n = 0;
-    const int rc = api([&] {
+    const int rc = api_ctx(ctx, [&] {
         resolve_stages(ctx);
         for (auto& [name, t] : ctx->stage_ms) {
             if (n >= cap) break;
@@ -557,51 +557,51 @@ int lo_context_stage_times(lo_context* ctx, char* names, int name_len, double* m
 }
 
 int lo_device_alloc(lo_context* ctx, uint64_t bytes, void** out_dev) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         *out_dev = dalloc(ctx, bytes);
         sync(ctx);
     });
 }
 int lo_device_free(lo_context* ctx, void* dev) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         dfree(ctx, dev);
         sync(ctx);
     });
 }
 int lo_memcpy_h2d(lo_context* ctx, void* dst, const void* src, uint64_t bytes) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         LO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
         sync(ctx);
     });
 }
 int lo_h2d_begin(lo_context* ctx, void* dst, const void* src, uint64_t bytes, int slot) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(slot >= 0 && slot < lo_context::kH2dSlots, LO_INVALID_ARGUMENT, "h2d slot out of range");
         LO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->h2d_stream));
         LO_CUDA(cudaEventRecord(ctx->h2d_done[slot], ctx->h2d_stream));
     });
 }
 int lo_h2d_wait(lo_context* ctx, int slot) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(slot >= 0 && slot < lo_context::kH2dSlots, LO_INVALID_ARGUMENT, "h2d slot out of range");
         LO_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->h2d_done[slot], 0));
     });
 }
 int lo_d2h_fence(lo_context* ctx, int slot) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(slot >= 0 && slot < lo_context::kH2dSlots, LO_INVALID_ARGUMENT, "d2h slot out of range");
         LO_CUDA(cudaEventRecord(ctx->d2h_done[slot], ctx->copy_stream));
     });
 }
 int lo_d2h_wait(lo_context* ctx, int slot) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(slot >= 0 && slot < lo_context::kH2dSlots, LO_INVALID_ARGUMENT, "d2h slot out of range");
         LO_CUDA(cudaEventSynchronize(ctx->d2h_done[slot]));
         reclaim(ctx, false);
     });
 }
 int lo_memcpy_d2h(lo_context* ctx, void* dst, const void* src, uint64_t bytes) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         LO_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
         sync(ctx);
     });
@@ -612,7 +612,7 @@ int lo_host_alloc_pinned(uint64_t bytes, void** out_host) {
 int lo_host_free_pinned(void* host) { return api([&] { LO_CUDA(cudaFreeHost(host)); }); }
 
 int lo_flush_l2(lo_context* ctx, void* scratch, uint64_t bytes) {
-    return api([&] { LO_CUDA(cudaMemsetAsync(scratch, 0x5a, bytes, ctx->stream)); });
+    return api_ctx(ctx, [&] { LO_CUDA(cudaMemsetAsync(scratch, 0x5a, bytes, ctx->stream)); });
 }
 
 }  // extern "C"

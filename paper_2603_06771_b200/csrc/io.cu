@@ -141,11 +141,11 @@ using namespace lo;
 extern "C" {
 
 int lo_reorder_pcb(lo_context* ctx, const char* path, int curve, int level, lo_coded** out) {
-    return api([&] { *out = reorder_pcb(ctx, path, curve, level); });
+    return api_ctx(ctx, [&] { *out = reorder_pcb(ctx, path, curve, level); });
 }
 
 int lo_coded_write_pcb(lo_context* ctx, const lo_coded* coded, const char* path) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(coded != nullptr && path != nullptr, LO_INVALID_ARGUMENT, "null cloud or path");
         const std::string p(path);
         std::vector<double> xyz(3 * coded->n);
@@ -165,7 +165,7 @@ int lo_coded_write_pcb(lo_context* ctx, const lo_coded* coded, const char* path)
 int lo_octree_from_leaves(lo_context* ctx, const lo_coded* coded, const uint64_t* boundaries_host,
                           const uint32_t* offsets_host, uint64_t count, const double disc_box[6],
                           int level, int curve, uint32_t n_max, lo_octree** out) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(boundaries_host && offsets_host && disc_box, LO_INVALID_ARGUMENT, "null leaf array");
         *out = octree_from_leaves(ctx, coded, boundaries_host, offsets_host, count, disc_box, level,
                                   curve, n_max);
@@ -173,7 +173,7 @@ int lo_octree_from_leaves(lo_context* ctx, const lo_coded* coded, const uint64_t
 }
 
 int lo_octree_save(lo_context* ctx, const lo_octree* tree, const char* path) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(tree != nullptr && path != nullptr, LO_INVALID_ARGUMENT, "null tree or path");
         const std::string p(path);
         const u64 count = tree->leaves + 1;
@@ -197,7 +197,7 @@ int lo_octree_save(lo_context* ctx, const lo_octree* tree, const char* path) {
 }
 
 int lo_octree_load(lo_context* ctx, const lo_coded* coded, const char* path, lo_octree** out) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(path != nullptr, LO_INVALID_ARGUMENT, "null path");
         const std::string p(path);
         File f(std::fopen(path, "rb"));

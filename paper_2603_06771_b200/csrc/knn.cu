@@ -458,7 +458,7 @@ extern "C" {
 
 int lo_knn(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32_t k,
            const uint32_t* centres_host, uint64_t m, int fingerprint, lo_knn_result** out) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(k >= 1, LO_INVALID_ARGUMENT, "knn: k must be >= 1");
         require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
         const u64 rows = centres_host ? m : coded->n;
@@ -480,7 +480,7 @@ int lo_knn(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32
 
 int lo_knn_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32_t k,
                   const double* queries_host, uint64_t m, lo_knn_result** out) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(k >= 1, LO_INVALID_ARGUMENT, "knn: k must be >= 1");
         require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
         ensure_float_shadows(ctx, coded, tree);
@@ -505,7 +505,7 @@ int lo_knn_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded,
 
 int lo_knn_range(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32_t k,
                  uint64_t begin, uint64_t end, int fingerprint, lo_knn_result** out) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(k >= 1, LO_INVALID_ARGUMENT, "knn: k must be >= 1");
         require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
         require(begin <= end && end <= coded->n, LO_INVALID_ARGUMENT, "centre range out of bounds");
@@ -526,7 +526,7 @@ int lo_knn_info_get(const lo_knn_result* res, uint64_t* rows, uint32_t* k_eff, d
 
 int lo_knn_download(lo_context* ctx, const lo_knn_result* res, uint32_t* idx_host, double* dist_host,
                     uint64_t* fingerprints_host) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         const u64 e = res->rows * res->keff;
         if (idx_host && e)
             LO_CUDA(cudaMemcpyAsync(idx_host, res->idx, 4 * e, cudaMemcpyDeviceToHost, ctx->stream));
@@ -542,8 +542,8 @@ int lo_knn_download(lo_context* ctx, const lo_knn_result* res, uint32_t* idx_hos
 }
 
 int lo_knn_destroy(lo_knn_result* res) {
-    return api([&] {
-        if (!res) return;
+    if (!res) return LO_OK;
+    return api_ctx(res->ctx, [&] {
         lo_context* ctx = res->ctx;
         dfree(ctx, res->idx);
         dfree(ctx, res->dist);
@@ -554,7 +554,7 @@ int lo_knn_destroy(lo_knn_result* res) {
 
 int lo_locality_log2(lo_context* ctx, const lo_knn_result* res, const lo_coded* coded,
                      const uint32_t* centres_host, int use_perm, uint64_t* bins33_host) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         u32* cidx = upload_centres(ctx, centres_host, centres_host ? res->rows : 0, coded->n);
         unsigned long long* bins = dalloc_t<unsigned long long>(ctx, 33);
         LO_CUDA(cudaMemsetAsync(bins, 0, 33 * 8, ctx->stream));
@@ -574,7 +574,7 @@ int lo_locality_log2(lo_context* ctx, const lo_knn_result* res, const lo_coded* 
 int lo_locality_histogram(lo_context* ctx, const lo_knn_result* res, const lo_coded* coded,
                           const uint32_t* centres_host, const uint32_t* index_map_host,
                           uint64_t* nbins, uint32_t* d_host, uint64_t* count_host, uint64_t cap) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(res && coded && nbins, LO_INVALID_ARGUMENT, "null argument");
         const u64 n = coded->n;
         u32* cidx = upload_centres(ctx, centres_host, centres_host ? res->rows : 0, n);

@@ -12,6 +12,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/linoct_b200.h"
@@ -131,6 +132,9 @@ struct lo_context {
     static constexpr int kH2dSlots = 4;
     cudaEvent_t h2d_done[kH2dSlots] = {};
     cudaEvent_t d2h_done[kH2dSlots] = {};  // lo_d2h_fence / lo_d2h_wait
+    // calls on one context are serialized; built handles stay safe to query from
+    // any thread
+    std::recursive_mutex mu;
 };
 
 struct lo_coded {
@@ -385,6 +389,14 @@ int api(F&& f) {
         set_last_error(e.what());
         return LO_LOGIC_ERROR;
     }
+}
+
+// api() under the context's lock.
+template <class F>
+int api_ctx(lo_context* ctx, F&& f) {
+    if (!ctx) return api([] { throw Error(LO_INVALID_ARGUMENT, "null context"); });
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
+    return api(std::forward<F>(f));
 }
 
 inline int ceil_div(u64 a, u64 b) { return static_cast<int>((a + b - 1) / b); }

@@ -677,7 +677,7 @@ extern "C" {
 int lo_build_leaves(lo_context* ctx, const uint64_t* codes_host, uint64_t n, uint32_t n_max,
                     int level, uint64_t* leaves, uint64_t* boundaries_host, uint32_t* offsets_host,
                     uint64_t cap) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(n_max >= 1, LO_INVALID_ARGUMENT, "build_leaves: n_max must be >= 1");
         require(n > 0, LO_INVALID_ARGUMENT, "build_leaves: empty code array");
         require(level >= 0 && level <= kMaxLevel, LO_INVALID_ARGUMENT, "level out of range");
@@ -710,7 +710,7 @@ int lo_build_leaves(lo_context* ctx, const uint64_t* codes_host, uint64_t n, uin
 }
 
 int lo_octree_build(lo_context* ctx, const lo_coded* coded, uint32_t n_max, lo_octree** out) {
-    return api([&] { *out = octree_build(ctx, coded, n_max); });
+    return api_ctx(ctx, [&] { *out = octree_build(ctx, coded, n_max); });
 }
 
 int lo_octree_info_get(const lo_octree* t, lo_octree_info* out) {
@@ -729,7 +729,7 @@ int lo_octree_info_get(const lo_octree* t, lo_octree_info* out) {
 
 int lo_octree_download(lo_context* ctx, const lo_octree* t, uint64_t* boundaries_host,
                        uint32_t* offsets_host, lo_internal_node* nodes_host) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         if (boundaries_host)
             LO_CUDA(cudaMemcpyAsync(boundaries_host, t->bounds, 8 * (t->leaves + 1),
                                     cudaMemcpyDeviceToHost, ctx->stream));
@@ -745,7 +745,7 @@ int lo_octree_download(lo_context* ctx, const lo_octree* t, uint64_t* boundaries
 
 int lo_octree_node_bounds(lo_context* ctx, const lo_octree* t, const int32_t* refs_host,
                           uint64_t count, double* boxes_host) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         if (count == 0) return;
         for (u64 r = 0; r < count; ++r) {
             const i32 ref = refs_host[r];
@@ -781,7 +781,7 @@ int lo_octree_device_ptrs(const lo_octree* t, void** boundaries, void** offsets,
 
 int lo_octree_create_empty(lo_context* ctx, const lo_coded* coded, const lo_octree_info* info,
                            lo_octree** out) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(coded && info && info->points == coded->n, LO_INVALID_ARGUMENT,
                 "octree header does not match the coded cloud");
         auto* t = new lo_octree;
@@ -812,8 +812,8 @@ int lo_octree_create_empty(lo_context* ctx, const lo_coded* coded, const lo_octr
 }
 
 int lo_octree_destroy(lo_octree* t) {
-    return api([&] {
-        if (!t) return;
+    if (!t) return LO_OK;
+    return api_ctx(t->ctx, [&] {
         lo_context* ctx = t->ctx;
         dfree(ctx, t->bounds);
         dfree(ctx, t->offsets);

@@ -351,7 +351,7 @@ extern "C" {
 int lo_radius(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int method, int shape,
               double radius, const uint32_t* centres_host, uint64_t m, int fingerprint,
               lo_csr** out) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(method != LO_METHOD_PTR, LO_INVALID_ARGUMENT,
                 "run_radius_batch: ptr method needs a pointer octree");
         require(method == LO_METHOD_LIN || method == LO_METHOD_PRUNE || method == LO_METHOD_STRUCT,
@@ -378,7 +378,7 @@ int lo_radius(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int
 
 int lo_radius_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int shape,
                      double radius, const double* queries_host, uint64_t m, lo_csr** out) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
         ensure_float_shadows(ctx, coded, tree);
         double *x = nullptr, *y = nullptr, *z = nullptr, bmax = 0.0;
@@ -402,7 +402,7 @@ int lo_radius_points(lo_context* ctx, const lo_octree* tree, const lo_coded* cod
 
 int lo_radius_struct_points(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int shape,
                             double radius, const double* queries_host, uint64_t m, lo_csr** out) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
         double *x = nullptr, *y = nullptr, *z = nullptr, bmax = 0.0;
         float4* f = nullptr;
@@ -425,7 +425,7 @@ int lo_radius_struct_points(lo_context* ctx, const lo_octree* tree, const lo_cod
 int lo_radius_range(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int method,
                     int shape, double radius, uint64_t begin, uint64_t end, int fingerprint,
                     lo_csr** out) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(method == LO_METHOD_LIN || method == LO_METHOD_PRUNE || method == LO_METHOD_STRUCT,
                 LO_INVALID_ARGUMENT, "unknown radius method");
         require(tree && coded, LO_INVALID_ARGUMENT, "null tree or cloud");
@@ -450,7 +450,7 @@ int lo_csr_info_get(const lo_csr* csr, lo_csr_info* out) {
 
 int lo_csr_download(lo_context* ctx, const lo_csr* csr, uint32_t* counts_host,
                     uint64_t* fingerprints_host, uint64_t* offsets_host, uint32_t* indices_host) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         if (csr->digested) LO_CUDA(cudaStreamWaitEvent(ctx->stream, csr->digested, 0));
         if (counts_host && csr->rows)
             LO_CUDA(cudaMemcpyAsync(counts_host, csr->counts, 4 * csr->rows, cudaMemcpyDeviceToHost,
@@ -474,7 +474,7 @@ int lo_csr_download(lo_context* ctx, const lo_csr* csr, uint32_t* counts_host,
 
 int lo_csr_download_async(lo_context* ctx, lo_csr* csr, uint32_t* counts_host,
                           uint64_t* fingerprints_host, uint64_t* offsets_host, uint32_t* indices_host) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(csr != nullptr, LO_INVALID_ARGUMENT, "null result");
         require(!fingerprints_host || csr->fps, LO_INVALID_ARGUMENT, "fingerprints were not computed");
         if (indices_host && csr->total) ensure_expanded(ctx, csr);
@@ -501,7 +501,8 @@ int lo_csr_download_async(lo_context* ctx, lo_csr* csr, uint32_t* counts_host,
 }
 
 int lo_csr_device_ptrs(const lo_csr* csr, const uint64_t** offsets, const uint32_t** indices) {
-    return api([&] {
+    if (!csr) return api([] { throw Error(LO_INVALID_ARGUMENT, "null result"); });
+    return api_ctx(csr->ctx, [&] {
         if (indices) ensure_expanded(csr->ctx, const_cast<lo_csr*>(csr));
         if (offsets) *offsets = csr->offsets;
         if (indices) *indices = csr->indices;
@@ -519,7 +520,7 @@ int lo_csr_struct_info(const lo_csr* csr, uint64_t* total_ranges, uint64_t* tota
 int lo_csr_struct_download(lo_context* ctx, const lo_csr* csr, uint64_t* range_offsets_host,
                            uint32_t* ranges_host, uint64_t* single_offsets_host,
                            uint32_t* singles_host) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(csr && csr->is_struct, LO_INVALID_ARGUMENT, "not a Struct radius result");
         if (range_offsets_host)
             LO_CUDA(cudaMemcpyAsync(range_offsets_host, csr->range_offsets, 8 * (csr->rows + 1),
@@ -538,8 +539,8 @@ int lo_csr_struct_download(lo_context* ctx, const lo_csr* csr, uint64_t* range_o
 }
 
 int lo_csr_destroy(lo_csr* csr) {
-    return api([&] {
-        if (!csr) return;
+    if (!csr) return LO_OK;
+    return api_ctx(csr->ctx, [&] {
         free_csr_buffers(csr->ctx, csr);
         delete csr;
     });

@@ -607,7 +607,7 @@ extern "C" {
 
 int lo_compute_codes(lo_context* ctx, const double* xyz_host, uint64_t n, int curve, int level,
                      const double* disc_box, uint64_t* codes_host) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(n > 0, LO_INVALID_ARGUMENT, "compute_codes: empty cloud");
         require(level >= 0 && level <= kMaxLevel, LO_INVALID_ARGUMENT, "level out of range");
         double* xyz = dalloc_t<double>(ctx, 3 * n);
@@ -644,7 +644,7 @@ int lo_compute_codes(lo_context* ctx, const double* xyz_host, uint64_t n, int cu
 
 int lo_encode_cells(lo_context* ctx, const uint32_t* cells_host, uint64_t n, int curve, int level,
                     uint64_t* codes_host) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(level >= 0 && level <= kMaxLevel, LO_INVALID_ARGUMENT, "level out of range");
         if (n == 0) return;
         u32* cells = dalloc_t<u32>(ctx, 3 * n);
@@ -664,7 +664,7 @@ int lo_encode_cells(lo_context* ctx, const uint32_t* cells_host, uint64_t n, int
 
 int lo_decode_codes(lo_context* ctx, const uint64_t* codes_host, uint64_t n, int curve, int level,
                     uint32_t* cells_host) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(level >= 0 && level <= kMaxLevel, LO_INVALID_ARGUMENT, "level out of range");
         if (n == 0) return;
         u64* codes = dalloc_t<u64>(ctx, n);
@@ -682,12 +682,12 @@ int lo_decode_codes(lo_context* ctx, const uint64_t* codes_host, uint64_t n, int
 
 int lo_reorder_device(lo_context* ctx, const double* xyz_dev, uint64_t n, int curve, int level,
                       lo_coded** out) {
-    return api([&] { *out = reorder_device(ctx, xyz_dev, n, curve, level); });
+    return api_ctx(ctx, [&] { *out = reorder_device(ctx, xyz_dev, n, curve, level); });
 }
 
 int lo_reorder(lo_context* ctx, const double* xyz_host, uint64_t n, int curve, int level,
                lo_coded** out) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(n > 0, LO_INVALID_ARGUMENT, "reorder_cloud: empty cloud");
         double* xyz = dalloc_t<double>(ctx, 3 * n);
         try {
@@ -717,7 +717,7 @@ int lo_coded_info_get(const lo_coded* c, lo_coded_info* out) {
 
 int lo_coded_download(lo_context* ctx, const lo_coded* c, double* xyz_host, uint64_t* codes_host,
                       uint32_t* perm_host) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         const u64 n = c->n;
         if (xyz_host) {
             double* aos = dalloc_t<double>(ctx, 3 * n);
@@ -746,8 +746,8 @@ int lo_coded_device_ptrs(const lo_coded* c, const double** x, const double** y, 
 }
 
 int lo_coded_destroy(lo_coded* c) {
-    return api([&] {
-        if (!c) return;
+    if (!c) return LO_OK;
+    return api_ctx(c->ctx, [&] {
         lo_context* ctx = c->ctx;
         dfree(ctx, c->x);
         dfree(ctx, c->y);
@@ -760,7 +760,7 @@ int lo_coded_destroy(lo_coded* c) {
 }
 
 int lo_coded_create_empty(lo_context* ctx, const lo_coded_info* info, lo_coded** out) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         require(info && info->n > 0 && info->n <= 0xffffffffull, LO_INVALID_ARGUMENT,
                 "coded cloud header: bad size");
         auto* c = new lo_coded;
@@ -789,7 +789,7 @@ int lo_coded_create_empty(lo_context* ctx, const lo_coded_info* info, lo_coded**
 }
 
 int lo_invert_permutation(lo_context* ctx, const uint32_t* perm_host, uint64_t n, uint32_t* inv_host) {
-    return api([&] {
+    return api_ctx(ctx, [&] {
         if (n == 0) return;
         u32* p = dalloc_t<u32>(ctx, n);
         u32* q = dalloc_t<u32>(ctx, n);

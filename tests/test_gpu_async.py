@@ -81,3 +81,36 @@ def test_pipelined_steps_with_d2h_fences(ctx, oracle):
     assert seen == 2
     with pytest.raises(Exception):
         _lib.check(L.lo_d2h_fence(ctx.h, 4))
+
+
+def test_concurrent_host_threads_share_a_context(ctx, oracle):
+    """Calls on one context are serialized by its lock: two host threads issuing radius
+    and kNN batches on the same context and structure get the sequential results."""
+    import threading
+    pts = oracle.gen_terrain(200000, 7, 150.0)
+    coded = lo.reorder_cloud(pts, lo.Curve.Hilbert)
+    tree = lo.LinearOctree(coded, 32)
+    want_r = lo.run_radius_batch(tree, coded, lo.RadiusMethod.Lin, lo.KernelShape.Sphere, 2.0, lo.BatchOptions())
+    want_k = lo.run_knn_batch(tree, coded, 16, lo.BatchOptions())
+    errors = []
+
+    def work(kind):
+        try:
+            for _ in range(3):
+                if kind == "radius":
+                    got = lo.run_radius_batch(tree, coded, lo.RadiusMethod.Lin, lo.KernelShape.Sphere, 2.0,
+                                              lo.BatchOptions())
+                    assert np.array_equal(got.counts, want_r.counts)
+                    assert np.array_equal(got.fingerprints, want_r.fingerprints)
+                else:
+                    got = lo.run_knn_batch(tree, coded, 16, lo.BatchOptions())
+                    assert np.array_equal(got.fingerprints, want_k.fingerprints)
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in ("radius", "knn", "radius")]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
