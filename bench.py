@@ -505,6 +505,11 @@ def run_ours(args, cfg):
         if b and st_ms > 0:
             rec = {"ms": round(st_ms, 4), "achieved_gbs": round(b / (st_ms * 1e-3) / 1e9, 1),
                    "frac": round(b / (st_ms * 1e-3) / 1e9 / PEAKS["hbm_gbs"], 4)}
+            name = st.partition("@r=")[0]
+            if name in ("bbox", "encode", "sort", "gather", "build"):  # keys/s per stage
+                rec["keys_per_s"] = round(n / (st_ms * 1e-3))
+            elif name in ("radius_count", "radius_fill"):
+                rec["queries_per_s"] = round(q / (st_ms * 1e-3))
             if st in traffic:
                 rec["traffic_gbs"] = round(traffic[st]["dram_bytes_per_launch"] / (st_ms * 1e-3) / 1e9, 1)
                 if traffic[st].get("issue_active_pct") is not None:
