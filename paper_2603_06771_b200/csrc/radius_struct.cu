@@ -90,7 +90,7 @@ struct StructShared {
 // the buffer lands in S.msk[L] (quads of queries per ballot round for the packed shapes).  Fill
 // walk: members of query L go to singles[srow_L + cursor] (coalesced per query).
 template <int SHAPE, int MODE>
-__device__ __forceinline__ void struct_buffer(StructShared& SS, u32 qmask, int lane, float lo_thr,
+__device__ __forceinline__ void struct_buffer(StructShared& SS, const float4 P, u32 qmask, int lane, float lo_thr,
                                               float hi_thr, const double* __restrict__ px,
                                               const double* __restrict__ py, const double* __restrict__ pz,
                                               double r, double r2, u32* __restrict__ singles, u64 srow,
@@ -98,7 +98,6 @@ __device__ __forceinline__ void struct_buffer(StructShared& SS, u32 qmask, int l
     constexpr bool FILL = MODE != 0;
     constexpr bool kPacked = SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE;
     PtShared& S = SS.pt;
-    const float4 P = S.buf[lane];
     const u32 idx = __float_as_uint(P.w);
     const u32 sw = SS.sw[lane];
     const u32 lt = (1u << lane) - 1u;
@@ -272,11 +271,19 @@ __global__ void __launch_bounds__(kPtThreads, 8) struct_pt_kernel(
         u32 fill = 0, qmask = 0, nrec = 0;
         u32* rec_tile = (MODE == 0 && rp.pool && chunk_left >= rp.cap) ? rp.pool + chunk_base * 64 : nullptr;
         auto flush = [&]() {
-            struct_buffer<SHAPE, MODE>(SS, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2, singles, srow, ns);
+            // the buffer's 32 points are loaded at once (one latency per buffer, not per leaf);
+            // slots >= fill get +INF coordinates and an empty want mask
+            float4 P = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+            if (static_cast<u32>(lane) < fill) {
+                const u32 g = S.bix[lane];
+                P = __ldg(pf + g);
+                P.w = __uint_as_float(g);
+            }
+            struct_buffer<SHAPE, MODE>(SS, P, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2, singles, srow, ns);
             if (MODE == 0 && rec_tile) {
                 if (nrec < rp.cap) {
                     u32* R = rec_tile + nrec * 64;
-                    R[lane] = __float_as_uint(S.buf[lane].w);
+                    R[lane] = __float_as_uint(P.w);
                     R[32 + lane] = S.msk[lane];
                 }
                 ++nrec;
@@ -346,9 +353,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) struct_pt_kernel(
                 const u32 take = min(32u - fill, nd.end - base);
                 __syncwarp();
                 if (static_cast<u32>(lane) < take) {
-                    float4 p = __ldg(pf + base + lane);
-                    p.w = __uint_as_float(base + lane);
-                    S.buf[fill + lane] = p;
+                    S.bix[fill + lane] = base + lane;
                     SS.sw[fill + lane] = inter;
                 }
                 fill += take;
@@ -364,10 +369,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) struct_pt_kernel(
         }
         if (fill) {
             __syncwarp();
-            if (static_cast<u32>(lane) >= fill) {
-                S.buf[lane] = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
-                SS.sw[lane] = 0;
-            }
+            if (static_cast<u32>(lane) >= fill) SS.sw[lane] = 0;
             __syncwarp();
             flush();
         }
@@ -539,7 +541,11 @@ static void launch_struct_pt(lo_context* ctx, int shape, const lo_octree* t, con
     LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
     const int pblocks = static_cast<int>(std::max<u64>(
         1, std::min<u64>((tiles + kPtWarps - 1) / kPtWarps, static_cast<u64>(ctx->sm_count) * 8)));
-    const float compact = static_cast<float>(4.0 * r);
+    static const double compact_mul = [] {  // as in the Lin walk (radius.cu)
+        const char* e = std::getenv("LO_COMPACT_MUL");
+        return e ? std::strtod(e, nullptr) : 8.0;
+    }();
+    const float compact = static_cast<float>(compact_mul * r);
 #define LO_STRUCT_PT(S)                                                                                 \
     case S:                                                                                             \
         struct_pt_kernel<S, MODE><<<pblocks, kPtThreads, 0, ctx->stream>>>(                             \
