@@ -1,0 +1,54 @@
+"""bench.py's JSON-line contract: every key the driver and the judge read, on the small cfg0 workload.
+The reference arm runs here on the CPU (oracle/_ref); our arm needs the B200."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+             "vs_baseline", "dtype", "data", "config"}
+
+
+def _run(args, timeout):
+    r = subprocess.run([sys.executable, "bench.py", *args], cwd=ROOT, capture_output=True, text=True,
+                       timeout=timeout)
+    assert r.returncode == 0, r.stderr[-4000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_reference_arm_contract():
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref")):
+        pytest.skip("reference library not built (python -c 'import __graft_entry__ as g; g.build()')")
+    d = _run(["--impl", "reference", "--config", "cfg0", "--steps", "1", "--warmup", "0"], 600)
+    assert d["impl"] == "reference"
+    assert BASE_KEYS <= d.keys()
+    assert d["value"] > 0 and d["unit"] == "queries/s" and d["higher_is_better"] is True
+    assert d["config"]["workload"] == "cfg0"
+    cb = d["cpu_baseline"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] == d["value"]
+    assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+def test_our_arm_contract():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a B200")
+    d = _run(["--config", "cfg0", "--steps", "3", "--warmup", "3"], 900)
+    assert BASE_KEYS <= d.keys()
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
+    assert d["config"]["workload"] == "cfg0"
+    rl = d["roofline"]
+    assert rl["bound"] in ("hbm", "tensor") and rl["peak"] > 0 and rl["unit"] == "GB/s"
+    assert abs(rl["frac"] - rl["achieved"] / rl["peak"]) < 1e-9 and "traffic" in rl
+    cb = d["cpu_baseline"]
+    assert cb["value"] > 0 and cb["cores"] >= 1 and cb["kind"] in ("reference", "port") and cb["sample"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
