@@ -205,9 +205,9 @@ def config_block(args, cfg):
     return {"workload": args.config, "points": cfg["n"], "cloud": cfg["kind"],
             "curve": "hilbert" if cfg["curve"] else "morton", "leaf_bucket": cfg["n_max"],
             "radii": cfg["radii"], "knn_k": cfg["ks"], "queries_per_step": len(cfg["radii"]) * cfg["n"],
-            "parallelism": (f"query-shard x{args.gpus} (" + ("structure broadcast from rank 0"
-                                                            if os.environ.get("LO_BENCH_BROADCAST") == "1"
-                                                            else "structure built on every rank") + ")")
+            "parallelism": (f"query-shard x{args.gpus} (" + ("structure built on every rank"
+                                                            if os.environ.get("LO_BENCH_REPLICATE") == "1"
+                                                            else "structure broadcast from rank 0") + ")")
             if args.gpus > 1 else "1 GPU",
             "l2": "inputs larger than L2 (cloud 24 B/pt + multi-GB CSR per step)"}
 
@@ -242,10 +242,11 @@ def run_ours(args, cfg):
     n = cfg["n"]
     radii = cfg["radii"]
 
-    # N > 1: every rank builds the (deterministic, bit-identical) structure from its own copy of the
-    # cloud -- 2.4 ms of reorder + build per step instead of the same on rank 0 plus a ~600 MB
-    # broadcast (SURVEY.md §8e step 1's alternative); LO_BENCH_BROADCAST=1 broadcasts from rank 0
-    replicate = world > 1 and os.environ.get("LO_BENCH_BROADCAST") != "1"
+    # N > 1: rank 0 builds and broadcasts the structure over NCCL (north star);
+    # LO_BENCH_REPLICATE=1 has every rank build the (deterministic, bit-identical) structure from its
+    # own copy of the cloud instead -- §8e's alternative, no communication (not measurable on the
+    # one-GPU boxes of this round)
+    replicate = world > 1 and os.environ.get("LO_BENCH_REPLICATE") == "1"
     builds = rank == 0 or replicate
     xyz_host = generate(cfg) if builds else None
     xyz_dev = C.c_void_p()

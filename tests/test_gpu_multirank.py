@@ -39,12 +39,12 @@ def test_sharded_search_equals_single_rank():
     assert "DIST_CHECK PASS" in r.stdout
 
 
-@pytest.mark.parametrize("broadcast", ["0", "1"])  # structure built on every rank / broadcast from rank 0
-def test_bench_two_ranks_contract(broadcast):
+@pytest.mark.parametrize("replicate", ["0", "1"])  # structure broadcast from rank 0 / built on every rank
+def test_bench_two_ranks_contract(replicate):
     r = _torchrun(["bench.py", "--gpus", "2", "--steps", "2", "--warmup", "1", "--no-cpu-baseline",
                    "--config", "cfg0"],
                   {"LO_BENCH_SAME_DEVICE": "1", "LO_BENCH_DIST_BACKEND": "gloo",
-                   "LO_BENCH_BROADCAST": broadcast}, 900)
+                   "LO_BENCH_REPLICATE": replicate}, 900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1  # rank 0 alone prints
