@@ -264,7 +264,11 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
         LO_CUDA(cudaEventRecord(e1, ctx->stream));
         if (fingerprint) {
             out->fps = big_alloc_t<u64>(ctx, q.m, &out->cap[1]);
-            if (q.m && !ctx->timing) {
+            // LO_DIGEST_AUX=1: the digests trail on the aux stream, overlapping the caller's next
+            // batch.  Off by default: with the count kernels issue-bound, the overlap cost more than
+            // it hid (cfg1 e2e 28.6 ms with it, 28.2 ms inline).
+            static const bool aux_digest = std::getenv("LO_DIGEST_AUX") != nullptr;
+            if (q.m && !ctx->timing && aux_digest) {
                 // the digests trail on the aux stream while the caller's next batch counts;
                 // readers of fps / indices (downloads, unsort, release) order behind `digested`
                 LO_CUDA(cudaStreamWaitEvent(ctx->aux_stream, e1, 0));
