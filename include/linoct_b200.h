@@ -263,6 +263,10 @@ int lo_knn_info_get(const lo_knn_result* res, uint64_t* rows, uint32_t* k_eff, d
 /* idx[m*k_eff], dist[m*k_eff], fingerprints[m]; NULL skips. */
 int lo_knn_download(lo_context* ctx, const lo_knn_result* res, uint32_t* idx_host, double* dist_host,
                     uint64_t* fingerprints_host);
+/* Same, asynchronously on the context's copy stream (pinned host buffers; filled once
+ * lo_context_synchronize / a later lo_d2h_wait returns); the result may be destroyed first. */
+int lo_knn_download_async(lo_context* ctx, lo_knn_result* res, uint32_t* idx_host, double* dist_host,
+                          uint64_t* fingerprints_host);
 int lo_knn_destroy(lo_knn_result* res);
 
 /* ---- locality histogram (locality.cpp:41-97), log2 bins ----------------------------- */

@@ -365,6 +365,22 @@ class RefPipeline:
                                            threads or self.threads, _ptr(counts), _ptr(fps))
         return wall, counts, fps
 
+    def radius_centres(self, r, centres, shape=0, method=1, threads=None):
+        """run_batch_loop's radius query over an explicit centre list; (wall s, counts, fps)."""
+        centres = np.ascontiguousarray(centres, np.uint32)
+        counts = np.empty(len(centres), np.uint32)
+        fps = np.empty(len(centres), np.uint64)
+        wall = self.ref.L.ref_radius_centres(self.h, method, shape, r, _ptr(centres), len(centres),
+                                             threads or self.threads, _ptr(counts), _ptr(fps))
+        return wall, counts, fps
+
+    def knn_centres(self, k, centres, threads=None):
+        centres = np.ascontiguousarray(centres, np.uint32)
+        fps = np.empty(len(centres), np.uint64)
+        wall = self.ref.L.ref_knn_centres(self.h, k, _ptr(centres), len(centres),
+                                          threads or self.threads, _ptr(fps))
+        return wall, fps
+
     def knn_range(self, k, begin, end, threads=None, digests=True):
         fps = np.empty(end - begin, np.uint64) if digests else None
         wall = self.ref.L.ref_knn_range(self.h, k, begin, end, threads or self.threads, _ptr(fps))
@@ -447,6 +463,10 @@ class Ref:
         L.ref_radius_range.restype = f64
         L.ref_knn_range.argtypes = [P, u32, u64, u64, C.c_int, P]
         L.ref_knn_range.restype = f64
+        L.ref_radius_centres.argtypes = [P, C.c_int, C.c_int, f64, P, u64, C.c_int, P, P]
+        L.ref_radius_centres.restype = f64
+        L.ref_knn_centres.argtypes = [P, u32, P, u64, C.c_int, P]
+        L.ref_knn_centres.restype = f64
 
     def max_threads(self):
         return self.L.ref_max_threads()

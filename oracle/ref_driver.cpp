@@ -485,6 +485,58 @@ double ref_radius_range(void* h, int method, int shape, double radius, std::uint
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// run_batch_loop (search.cpp:287-312) over an explicit list of centre indices instead of
+// batch_centers(): the query of run_radius_batch (search.cpp:322-350, Lin/Prune, FNV digests
+// on) for every listed centre, dynamic OpenMP schedule, counts/digests in list order.  The
+// bench's reference arm passes many contiguous SFC slices spread over the whole cloud, so a
+// bounded sample sees every part of the cloud (clusters, terrain, noise) in proportion.
+// Returns the loop's wall seconds (steady_clock, as run_batch_loop measures).
+double ref_radius_centres(void* h, int method, int shape, double radius, const std::uint32_t* centres,
+                          std::uint64_t m, int threads, std::uint32_t* counts, std::uint64_t* fps) {
+    auto* p = static_cast<Pipeline*>(h);
+    const auto t0 = std::chrono::steady_clock::now();
+#pragma omp parallel for schedule(dynamic) num_threads(threads)
+    for (std::int64_t i = 0; i < static_cast<std::int64_t>(m); ++i) {
+        thread_local std::vector<std::uint32_t> idx;
+        const SearchKernel kernel(static_cast<KernelShape>(shape), p->coded.cloud[centres[i]], radius);
+        if (method == 2) neighbours_prune(*p->tree, p->coded, kernel, idx);
+        else neighbours_lin(*p->tree, p->coded, kernel, idx);
+        std::uint64_t hsh = 0xcbf29ce484222325ULL;
+        for (std::uint32_t v : idx) {
+            for (int b = 0; b < 8; ++b) {
+                hsh ^= (static_cast<std::uint64_t>(v) >> (8 * b)) & 0xff;
+                hsh *= 0x100000001b3ULL;
+            }
+        }
+        if (counts) counts[i] = static_cast<std::uint32_t>(idx.size());
+        if (fps) fps[i] = hsh;
+    }
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// run_knn_batch's query (search.cpp:369-388) over an explicit centre list, digests on.
+double ref_knn_centres(void* h, std::uint32_t k, const std::uint32_t* centres, std::uint64_t m,
+                       int threads, std::uint64_t* fps) {
+    auto* p = static_cast<Pipeline*>(h);
+    const auto t0 = std::chrono::steady_clock::now();
+#pragma omp parallel for schedule(dynamic) num_threads(threads)
+    for (std::int64_t i = 0; i < static_cast<std::int64_t>(m); ++i) {
+        thread_local std::vector<KnnNeighbor> found;
+        knn_lin_oct(*p->tree, p->coded, p->coded.cloud[centres[i]], k, found);
+        std::uint64_t hsh = 0xcbf29ce484222325ULL;
+        for (const KnnNeighbor& nb : found) {
+            const std::uint64_t vals[2] = {nb.index, std::bit_cast<std::uint64_t>(nb.dist_sq)};
+            for (std::uint64_t v : vals)
+                for (int b = 0; b < 8; ++b) {
+                    hsh ^= (v >> (8 * b)) & 0xff;
+                    hsh *= 0x100000001b3ULL;
+                }
+        }
+        if (fps) fps[i] = hsh;
+    }
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 // knn_lin_oct over [begin, end) (search.cpp:369-388 restricted to a slice).
 double ref_knn_range(void* h, std::uint32_t k, std::uint64_t begin, std::uint64_t end, int threads,
                      std::uint64_t* fps) {

@@ -97,6 +97,7 @@ SIGNATURES = {
     "lo_knn_range": (cint, [P, P, P, u32, u64, u64, cint, PP]),
     "lo_knn_info_get": (cint, [P, P, P, P]),
     "lo_knn_download": (cint, [P, P, P, P, P]),
+    "lo_knn_download_async": (cint, [P, P, P, P, P]),
     "lo_knn_destroy": (cint, [P]),
     "lo_locality_log2": (cint, [P, P, P, P, cint, P]),
     "lo_generate_uniform": (cint, [u64, u64, f64, P]),

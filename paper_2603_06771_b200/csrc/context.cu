@@ -492,6 +492,11 @@ int lo_context_create(int device, void* stream, lo_context** out) {
 int lo_context_destroy(lo_context* ctx) {
     return api([&] {
         if (!ctx) return;
+        const int live = ctx->live_handles.load();
+        if (live > 0)
+            throw Error(LO_LOGIC_ERROR, "lo_context_destroy: " + std::to_string(live) +
+                                            " handle(s) created on this context are still alive");
+        DeviceGuard dev(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
         if (ctx->aux_stream) cudaStreamSynchronize(ctx->aux_stream);

@@ -300,6 +300,46 @@ __global__ void locality_dense(const u32* __restrict__ idx, u64 m, u32 keff,
         if (sh[i]) atomicAdd(&dense[i], static_cast<unsigned long long>(sh[i]));
 }
 
+// Sparse path (index maps whose value span exceeds the dense array): every pair's d as a u64
+// key, then sort + run-length encode.
+__global__ void locality_pairs(const u32* __restrict__ idx, u64 m, u32 keff, const u32* __restrict__ centres,
+                               const u32* __restrict__ map, u64* __restrict__ keys, u32* __restrict__ hist) {
+    __shared__ u32 h[4 * 256];
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < m * keff; e += (u64)gridDim.x * blockDim.x) {
+        const u64 r = e / keff;
+        const u32 ci = centres ? centres[r] : static_cast<u32>(r);
+        const u32 mi = map[ci], mj = map[idx[e]];
+        const u32 d = mi > mj ? mi - mj : mj - mi;
+        keys[e] = d;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) atomicAdd(&h[b * 256 + ((d >> (8 * b)) & 0xffu)], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+__global__ void run_heads(const u64* __restrict__ ks, u64 n, u32* __restrict__ f) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        f[i] = i == 0 || ks[i] != ks[i - 1];
+}
+
+__global__ void run_emit(const u64* __restrict__ ks, const u64* __restrict__ pos, u64 n, u32* __restrict__ d_out,
+                         u64* __restrict__ start) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        if (i == 0 || ks[i] != ks[i - 1]) {
+            d_out[pos[i]] = static_cast<u32>(ks[i]);
+            start[pos[i]] = i;
+        }
+}
+
+__global__ void run_lengths(const u64* __restrict__ start, u64 nb, u64 n, u64* __restrict__ c_out) {
+    for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < nb; j += (u64)gridDim.x * blockDim.x)
+        c_out[j] = (j + 1 < nb ? start[j + 1] : n) - start[j];
+}
+
 __global__ void nonzero_flags(const unsigned long long* __restrict__ dense, u64 n, u32* __restrict__ f) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
         f[i] = dense[i] != 0;
@@ -339,7 +379,7 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
         LO_CUDA(cudaEventRecord(e0, ctx->stream));
         out->idx = dalloc_t<u32>(ctx, q.m * kh);
         out->dist = dalloc_t<double>(ctx, q.m * kh);
-        const bool use_float = q.f && t->tf && c->pf;
+        const bool use_float = q.f && t->tf && c->pf && !force_fp64();
         // FP32-filtered kernel: (key f32, index) heap entries; exact fallback: (f64, index)
         const bool keyed = use_float && kh >= 32;  // compact heap entries where occupancy binds
         const size_t per_warp_heap = static_cast<size_t>(kh) * 32 * (keyed ? 8 : 12);
@@ -541,13 +581,49 @@ int lo_knn_download(lo_context* ctx, const lo_knn_result* res, uint32_t* idx_hos
     });
 }
 
+// Same as lo_knn_download, asynchronously on the context's copy stream (pinned host buffers):
+// the next batch computes while these rows travel; the result may be destroyed before the
+// copy lands (its buffers are released behind it).
+int lo_knn_download_async(lo_context* ctx, lo_knn_result* res, uint32_t* idx_host, double* dist_host,
+                          uint64_t* fingerprints_host) {
+    return api_ctx(ctx, [&] {
+        require(res != nullptr, LO_INVALID_ARGUMENT, "null result");
+        require(!fingerprints_host || !res->rows || res->fps, LO_INVALID_ARGUMENT, "fingerprints were not computed");
+        if (!res->copied) LO_CUDA(cudaEventCreateWithFlags(&res->copied, cudaEventDisableTiming));
+        cudaEvent_t ready;
+        LO_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        LO_CUDA(cudaEventRecord(ready, ctx->stream));
+        LO_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
+        cudaEventDestroy(ready);  // released once the recorded work completes
+        const cudaStream_t s = ctx->copy_stream;
+        const u64 e = res->rows * res->keff;
+        if (idx_host && e) LO_CUDA(cudaMemcpyAsync(idx_host, res->idx, 4 * e, cudaMemcpyDeviceToHost, s));
+        if (dist_host && e) LO_CUDA(cudaMemcpyAsync(dist_host, res->dist, 8 * e, cudaMemcpyDeviceToHost, s));
+        if (fingerprints_host && res->rows)
+            LO_CUDA(cudaMemcpyAsync(fingerprints_host, res->fps, 8 * res->rows, cudaMemcpyDeviceToHost, s));
+        LO_CUDA(cudaEventRecord(res->copied, s));
+    });
+}
+
 int lo_knn_destroy(lo_knn_result* res) {
     if (!res) return LO_OK;
     return api_ctx(res->ctx, [&] {
         lo_context* ctx = res->ctx;
-        dfree(ctx, res->idx);
-        dfree(ctx, res->dist);
-        dfree(ctx, res->fps);
+        bool pending = false;
+        if (res->copied) {
+            pending = cudaEventQuery(res->copied) != cudaSuccess;
+            if (pending) cudaGetLastError();  // cudaErrorNotReady is not an error
+            cudaEventDestroy(res->copied);
+        }
+        if (pending) {  // an async download still reads them: release behind the copy stream
+            big_release(ctx, res->idx, 0, ctx->copy_stream);
+            big_release(ctx, res->dist, 0, ctx->copy_stream);
+            big_release(ctx, res->fps, 0, ctx->copy_stream);
+        } else {
+            dfree(ctx, res->idx);
+            dfree(ctx, res->dist);
+            dfree(ctx, res->fps);
+        }
         delete res;
     });
 }
@@ -589,30 +665,92 @@ int lo_locality_histogram(lo_context* ctx, const lo_knn_result* res, const lo_co
             dfree(ctx, dd), dfree(ctx, cc);
         };
         try {
+            // d = |map(i) - map(j)| < span of the map's values (any u32 is a legal map value,
+            // locality.cpp:47-49): a dense array over [0, span) when that is small enough, else
+            // sort + run-length encode the pairs' d
+            u64 span = n;
+            if (index_map_host && n) {
+                const auto mm = std::minmax_element(index_map_host, index_map_host + n);
+                span = static_cast<u64>(*mm.second) - *mm.first + 1;
+            }
             if (index_map_host) {
                 map = dalloc_t<u32>(ctx, n);
                 LO_CUDA(cudaMemcpyAsync(map, index_map_host, 4 * n, cudaMemcpyHostToDevice, ctx->stream));
             }
-            dense = dalloc_t<unsigned long long>(ctx, n);
-            LO_CUDA(cudaMemsetAsync(dense, 0, 8 * n, ctx->stream));
+            const u64 pairs = res->rows * res->keff;
+            if (span > std::max<u64>(n, 1ull << 27)) {
+                require(pairs < (1ull << 32), LO_INVALID_ARGUMENT,
+                        "locality histogram: too many pairs for a sparse index map");
+                u64* keys = dalloc_t<u64>(ctx, pairs);
+                u64* ks = nullptr;
+                u32* perm = nullptr;
+                u32* hist = nullptr;
+                u64* start = nullptr;
+                try {
+                    ks = dalloc_t<u64>(ctx, pairs);
+                    perm = dalloc_t<u32>(ctx, pairs);
+                    hist = dalloc_t<u32>(ctx, 4 * 256);
+                    LO_CUDA(cudaMemsetAsync(hist, 0, 4 * 256 * 4, ctx->stream));
+                    const int g = std::max(1, std::min(ceil_div(pairs, 256), ctx->sm_count * 8));
+                    if (pairs) {
+                        locality_pairs<<<g, 256, 0, ctx->stream>>>(res->idx, res->rows, res->keff, cidx, map, keys,
+                                                                 hist);
+                        LO_CHECK_LAUNCH();
+                    }
+                    std::vector<u32> hh(8 * 256, 0);
+                    fetch_small(ctx, hist, 4 * 256 * 4);
+                    std::memcpy(hh.data(), ctx->pinned_scratch, 4 * 256 * 4);
+                    hh[4 * 256] = static_cast<u32>(pairs);  // bits 32..39 are zero
+                    if (pairs) radix_sort(ctx, keys, pairs, hh.data(), 11, ks, perm);
+                    flags = dalloc_t<u32>(ctx, pairs);
+                    pos = dalloc_t<u64>(ctx, pairs + 1);
+                    run_heads<<<g, 256, 0, ctx->stream>>>(ks, pairs, flags);
+                    LO_CHECK_LAUNCH();
+                    exclusive_scan_u32_to_u64(ctx, flags, pos, pairs);
+                    const u64 nb = read_scalar(ctx, pos + pairs);
+                    *nbins = nb;
+                    if (d_host && count_host && nb <= cap && nb) {
+                        dd = dalloc_t<u32>(ctx, nb);
+                        cc = dalloc_t<u64>(ctx, nb);
+                        start = dalloc_t<u64>(ctx, nb);
+                        run_emit<<<g, 256, 0, ctx->stream>>>(ks, pos, pairs, dd, start);
+                        LO_CHECK_LAUNCH();
+                        run_lengths<<<std::max(1, std::min(ceil_div(nb, 256), ctx->sm_count * 8)), 256, 0,
+                                      ctx->stream>>>(start, nb, pairs, cc);
+                        LO_CHECK_LAUNCH();
+                        LO_CUDA(cudaMemcpyAsync(d_host, dd, 4 * nb, cudaMemcpyDeviceToHost, ctx->stream));
+                        LO_CUDA(cudaMemcpyAsync(count_host, cc, 8 * nb, cudaMemcpyDeviceToHost, ctx->stream));
+                    }
+                    sync(ctx);
+                } catch (...) {
+                    dfree(ctx, keys), dfree(ctx, ks), dfree(ctx, perm), dfree(ctx, hist), dfree(ctx, start);
+                    throw;
+                }
+                dfree(ctx, keys), dfree(ctx, ks), dfree(ctx, perm), dfree(ctx, hist), dfree(ctx, start);
+                release();
+                return;
+            }
+            const u64 dn = span;  // dense bins over [0, span)
+            dense = dalloc_t<unsigned long long>(ctx, dn);
+            LO_CUDA(cudaMemsetAsync(dense, 0, 8 * dn, ctx->stream));
             const u64 e = res->rows * res->keff;
             if (e) {
                 locality_dense<<<std::max(1, std::min(ceil_div(e, 256), ctx->sm_count * 4)), 256, 0,
                                  ctx->stream>>>(res->idx, res->rows, res->keff, cidx, map, dense);
                 LO_CHECK_LAUNCH();
             }
-            flags = dalloc_t<u32>(ctx, n);
-            pos = dalloc_t<u64>(ctx, n + 1);
-            const int g = std::max(1, std::min(ceil_div(n, 256), ctx->sm_count * 16));
-            nonzero_flags<<<g, 256, 0, ctx->stream>>>(dense, n, flags);
+            flags = dalloc_t<u32>(ctx, dn);
+            pos = dalloc_t<u64>(ctx, dn + 1);
+            const int g = std::max(1, std::min(ceil_div(dn, 256), ctx->sm_count * 16));
+            nonzero_flags<<<g, 256, 0, ctx->stream>>>(dense, dn, flags);
             LO_CHECK_LAUNCH();
-            exclusive_scan_u32_to_u64(ctx, flags, pos, n);
-            const u64 nb = read_scalar(ctx, pos + n);
+            exclusive_scan_u32_to_u64(ctx, flags, pos, dn);
+            const u64 nb = read_scalar(ctx, pos + dn);
             *nbins = nb;
             if (d_host && count_host && nb <= cap && nb) {
                 dd = dalloc_t<u32>(ctx, nb);
                 cc = dalloc_t<u64>(ctx, nb);
-                compact_bins<<<g, 256, 0, ctx->stream>>>(dense, pos, n, dd, cc);
+                compact_bins<<<g, 256, 0, ctx->stream>>>(dense, pos, dn, dd, cc);
                 LO_CHECK_LAUNCH();
                 LO_CUDA(cudaMemcpyAsync(d_host, dd, 4 * nb, cudaMemcpyDeviceToHost, ctx->stream));
                 LO_CUDA(cudaMemcpyAsync(count_host, cc, 8 * nb, cudaMemcpyDeviceToHost, ctx->stream));

@@ -8,10 +8,12 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -135,10 +137,42 @@ struct lo_context {
     // calls on one context are serialized; built handles stay safe to query from
     // any thread
     std::recursive_mutex mu;
+    // handles (coded, octree, csr, knn) that still point here: destroying the context first is a
+    // LO_LOGIC_ERROR instead of a use-after-free in their destroy calls
+    std::atomic<int> live_handles{0};
+    // kernels whose dynamic shared-memory limit was raised on this context's device (function
+    // attributes are per device; the flag lives under the context lock)
+    unsigned smem_attrs = 0;
 };
 
+namespace lo {
+// A handle's owning context, counted in lo_context::live_handles while it is set.
+class CtxRef {
+  public:
+    CtxRef() = default;
+    CtxRef(const CtxRef&) = delete;
+    CtxRef& operator=(const CtxRef&) = delete;
+    ~CtxRef() { reset(nullptr); }
+    CtxRef& operator=(lo_context* c) {
+        reset(c);
+        return *this;
+    }
+    operator lo_context*() const { return p_; }
+    lo_context* operator->() const { return p_; }
+
+  private:
+    void reset(lo_context* c) {
+        if (p_) p_->live_handles.fetch_sub(1);
+        p_ = c;
+        if (p_) p_->live_handles.fetch_add(1);
+    }
+    lo_context* p_ = nullptr;
+};
+}  // namespace lo
+
 struct lo_coded {
-    lo_context* ctx = nullptr;
+    lo::CtxRef ctx;
+    std::mutex lazy_mu;  // lazily built device data (ensure_float_shadows) is published under it
     lo::u64 n = 0;
     int curve = 0, level = lo::kMaxLevel;
     double disc_box[6] = {};
@@ -154,7 +188,8 @@ struct lo_coded {
 };
 
 struct lo_octree {
-    lo_context* ctx = nullptr;
+    lo::CtxRef ctx;
+    std::mutex lazy_mu;  // lazily built tf / rb / rbf are published under it, complete
     const lo_coded* coded = nullptr;
     lo::u64 points = 0, leaves = 0, internal = 0, tnodes = 0;
     lo::i32 root = 0;
@@ -180,7 +215,7 @@ void ensure_ref_boxes(lo_context* ctx, const lo_coded* coded, const lo_octree* t
 }  // namespace lo
 
 struct lo_csr {
-    lo_context* ctx = nullptr;
+    lo::CtxRef ctx;
     lo::u64 rows = 0, total = 0;
     double mean = 0.0;
     float ms = 0.f;
@@ -239,13 +274,14 @@ void free_csr_buffers(lo_context* ctx, lo_csr* csr);
 }  // namespace lo
 
 struct lo_knn_result {
-    lo_context* ctx = nullptr;
+    lo::CtxRef ctx;
     lo::u64 rows = 0;
     lo::u32 k = 0, keff = 0;
     float ms = 0.f;
     lo::u32* idx = nullptr;      // [rows*keff]
     double* dist = nullptr;      // [rows*keff]
     lo::u64* fps = nullptr;      // [rows] or null
+    cudaEvent_t copied = nullptr; // last lo_knn_download_async (null: none pending)
 };
 
 namespace lo {
@@ -391,14 +427,60 @@ int api(F&& f) {
     }
 }
 
-// api() under the context's lock.
+// Makes `device` current for the scope (a context may be used from any host thread, whose
+// current device can be another one) and restores the caller's device afterwards.
+class DeviceGuard {
+  public:
+    explicit DeviceGuard(int device) {
+        if (cudaGetDevice(&prev_) != cudaSuccess) {
+            cudaGetLastError();
+            prev_ = -1;
+        }
+        if (prev_ != device) {
+            cudaSetDevice(device);
+        } else {
+            prev_ = -1;
+        }
+    }
+    ~DeviceGuard() {
+        if (prev_ >= 0) cudaSetDevice(prev_);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+
+  private:
+    int prev_ = -1;
+};
+
+// api() under the context's lock, on the context's device.
 template <class F>
 int api_ctx(lo_context* ctx, F&& f) {
     if (!ctx) return api([] { throw Error(LO_INVALID_ARGUMENT, "null context"); });
     std::lock_guard<std::recursive_mutex> lock(ctx->mu);
+    DeviceGuard dev(ctx->device);
     return api(std::forward<F>(f));
 }
 
+// Raises a kernel's dynamic shared-memory limit once per context (= per device).
+enum : unsigned { kAttrSort = 1u, kAttrReplay = 2u };
+template <class K>
+void ensure_smem_attr(lo_context* ctx, unsigned bit, K kernel, size_t smem) {
+    if (ctx->smem_attrs & bit) return;
+    LO_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    ctx->smem_attrs |= bit;
+}
+
 inline int ceil_div(u64 a, u64 b) { return static_cast<int>((a + b - 1) / b); }
+
+// Test knobs, read on every call (not cached) so a test can flip them between calls:
+//   LO_FORCE_FP64=1      every search takes its exact FP64 kernel (the FP32 filter off), the path
+//                        radii below ~2.4e-5 x the cube side take on their own
+//   LO_RADIUS_NO_FUSE=1  radius fill by a second walk instead of replaying count-pass records
+//   LO_REC_CAP=<n>       records per tile before a tile overflows to the fill walk (default 128)
+inline bool env_flag(const char* name) {
+    const char* e = std::getenv(name);
+    return e && *e && *e != '0';
+}
+inline bool force_fp64() { return env_flag("LO_FORCE_FP64"); }
 
 }  // namespace lo

@@ -271,9 +271,24 @@ static void build_float_nodes(lo_context* ctx, lo_octree* t, const lo_coded* c) 
     LO_CHECK_LAUNCH();
 }
 
+// Lazily built device data is published complete: built under the handle's own mutex and
+// synchronized before the lock is released, so another context sharing the (read-only) handle
+// never sees a pointer whose kernels are still running on the builder's stream.
 void ensure_float_shadows(lo_context* ctx, const lo_coded* coded, const lo_octree* tree) {
-    build_float_points(ctx, const_cast<lo_coded*>(coded));
-    build_float_nodes(ctx, const_cast<lo_octree*>(tree), coded);
+    auto* c = const_cast<lo_coded*>(coded);
+    auto* t = const_cast<lo_octree*>(tree);
+    {
+        std::lock_guard<std::mutex> g(c->lazy_mu);
+        if (!c->pf) {
+            build_float_points(ctx, c);
+            sync(ctx);
+        }
+    }
+    std::lock_guard<std::mutex> g(t->lazy_mu);
+    if (!t->tf) {
+        build_float_nodes(ctx, t, coded);
+        sync(ctx);
+    }
 }
 
 // node_bounds (linear_octree.cpp:139-147): padded octant box of a NodeRef.
@@ -377,6 +392,7 @@ __global__ void ref_boxes_float(const double* __restrict__ rb, u64 count, double
 
 void ensure_ref_boxes(lo_context* ctx, const lo_coded* coded, const lo_octree* tree) {
     auto* t = const_cast<lo_octree*>(tree);
+    std::lock_guard<std::mutex> g(t->lazy_mu);  // published complete (see ensure_float_shadows)
     if (t->rb && t->rbf) return;
     const u64 T = t->tnodes;
     u8* depth = dalloc_t<u8>(ctx, T);
@@ -408,6 +424,7 @@ void ensure_ref_boxes(lo_context* ctx, const lo_coded* coded, const lo_octree* t
         throw;
     }
     dfree(ctx, depth);
+    sync(ctx);
     t->rb = rb;
 }
 

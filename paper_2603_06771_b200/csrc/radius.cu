@@ -131,8 +131,9 @@ struct RecArgs {  // count-pass records for the replay fill (radius_pt.cuh)
 };
 
 static bool float_path(const lo_octree* t, const lo_coded* c, const Queries& q, double r) {
-    return make_float_test(r, std::max(c->bmax, q.bmax)).enabled && q.f && t->tf && c->pf;
+    return make_float_test(r, std::max(c->bmax, q.bmax)).enabled && q.f && t->tf && c->pf && !force_fp64();
 }
+
 
 template <bool FILL>
 static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const lo_coded* c,
@@ -221,10 +222,11 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
         out->counts = big_alloc_t<u32>(ctx, q.m, &out->cap[0]);
         out->offsets = big_alloc_t<u64>(ctx, q.m + 1, &out->cap[2]);
         const u64 tiles = (q.m + 31) / 32;
-        static const bool no_fuse = std::getenv("LO_RADIUS_NO_FUSE") != nullptr;
+        const bool no_fuse = env_flag("LO_RADIUS_NO_FUSE");
+        const u32 cap = rec_cap();
         if (q.m && !no_fuse && float_path(t, c, q, r)) {
             try {
-                RecSetup rs = setup_records(ctx, tiles, kRecCap);
+                RecSetup rs = setup_records(ctx, tiles, cap);
                 ra.rp = rs.rp;
                 ovf = rs.ovf;
                 ovf_n = rs.ovf_n;
@@ -248,7 +250,7 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
             static const bool debug = std::getenv("LO_DEBUG") != nullptr;
             if (debug)
                 std::fprintf(stderr, "[lo] radius r=%g: %u of %llu tiles overflowed the %u-buffer records\n",
-                             r, n_ovf, static_cast<unsigned long long>(tiles), kRecCap);
+                             r, n_ovf, static_cast<unsigned long long>(tiles), cap);
             if (n_ovf) {
                 RecArgs fb;
                 fb.list = ovf;

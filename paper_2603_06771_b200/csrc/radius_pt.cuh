@@ -375,6 +375,12 @@ static __global__ void __launch_bounds__(32 * kReplayWarps, kReplayBlocks) radiu
 
 // Max records per tile for the fused count -> replay fill (128 buffers x 256 B = 32 KB).
 constexpr u32 kRecCap = 128;
+// LO_REC_CAP (test knob, read per call): a smaller per-tile record cap forces the overflow path
+inline u32 rec_cap() {
+    const char* e = std::getenv("LO_REC_CAP");
+    const unsigned long v = e ? std::strtoul(e, nullptr, 10) : 0;
+    return v >= 1 && v <= kRecCap ? static_cast<u32>(v) : kRecCap;
+}
 
 // The count pass's record pool in the persistent context arena: rec_off[tiles] u64 | alloc u64 |
 // rec_n[tiles] | overflow list[tiles] | ovf_n | pool (records of 256 B).  The pool is sized for
@@ -471,12 +477,7 @@ static inline u32 replay_records(lo_context* ctx, const RecSetup& rs, u64 m, con
             1, std::min<u64>((tiles + kReplayWarps - 1) / kReplayWarps, ctx->sm_count * 16ull)));
         radius_replay_bm_kernel<<<rb, 128, 0, ctx->stream>>>(rs.rp, m, offsets, out, rs.ovf, rs.ovf_n);
     } else {
-        static const bool attr = [] {
-            LO_CUDA(cudaFuncSetAttribute(radius_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kReplaySmem)));
-            return true;
-        }();
-        (void)attr;
+        ensure_smem_attr(ctx, kAttrReplay, radius_replay_kernel, kReplaySmem);
         const int rr = static_cast<int>(std::max<u64>(
             1, std::min<u64>((tiles + kReplayWarps - 1) / kReplayWarps, ctx->sm_count * static_cast<u64>(kReplayBlocks))));
         radius_replay_kernel<<<rr, 32 * kReplayWarps, kReplaySmem, ctx->stream>>>(rs.rp, m, offsets, out, rs.ovf,

@@ -526,7 +526,8 @@ static int grid_rows(lo_context* ctx, u64 m) {
 }
 
 static bool struct_float_path(const lo_octree* t, const lo_coded* c, const Queries& q, double r) {
-    return make_float_test(r, std::max(c->bmax, q.bmax)).enabled && q.f && t->tf && c->pf && t->rbf;
+    return make_float_test(r, std::max(c->bmax, q.bmax)).enabled && q.f && t->tf && c->pf && t->rbf &&
+           !force_fp64();
 }
 
 // MODE 0 count (+ records, range slots), 2 full fill walk (over `list` when given).
@@ -618,7 +619,7 @@ lo_csr* radius_struct_search(lo_context* ctx, const lo_octree* t, const lo_coded
         RecSetup rs;
         if (fast) {
             try {
-                rs = setup_records(ctx, (q.m + 31) / 32, kRecCap);
+                rs = setup_records(ctx, (q.m + 31) / 32, rec_cap());
                 rscratch = dalloc_t<u32>(ctx, 2 * q.m * kStructRangeCap);
             } catch (const Error&) {  // no room for records / range slots: fill walks instead
                 rs = RecSetup{};

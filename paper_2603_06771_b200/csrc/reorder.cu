@@ -447,13 +447,10 @@ void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int lev
     // ping-pong so that the final pass lands in (keys_sorted, perm)
     const int np = static_cast<int>(run.size());
     const size_t smem = sizeof(SortSmem);
-    static bool attr_set = false;
-    if (!attr_set) {
+    if (!(ctx->smem_attrs & kAttrSort)) {
         LO_CUDA(cudaFuncSetAttribute(onesweep_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-        LO_CUDA(cudaFuncSetAttribute(onesweep_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-        attr_set = true;
+        ensure_smem_attr(ctx, kAttrSort, onesweep_pass<false>, smem);
     }
     const u64* kin = keys;
     const u32* vin = nullptr;
