@@ -359,9 +359,16 @@ class Arm:
             _lib.check(L.lo_memcpy_h2d(ctx.h, self.xyz_dev, self.xyz_host.ctypes.data, 24 * self.n))
         from paper_2603_06771_b200 import distributed as D
         self.D = D
-        self.b0, self.b1 = D.shard_range(self.n, rank, world)
+        # N > 1 over NCCL: the library's own communicator (lo_comm, C ABI) broadcasts the structure
+        # and shards the searches; the gloo test hook (several ranks on one device, where NCCL
+        # refuses duplicate GPUs) keeps the torch.distributed plumbing
+        self.comm = None
+        if world > 1 and not replicate and os.environ.get("LO_BENCH_DIST_BACKEND", "nccl") == "nccl":
+            self.comm = D.Comm(ctx, rank, world)
+        self.b0, self.b1 = self.comm.shard(self.n) if self.comm else D.shard_range(self.n, rank, world)
         self.totals = {}
-        self.bcast_ms = []
+        self.global_totals = {}
+        self.bcast_last_ms = 0.0
 
     def check(self, rc):
         self._lib.check(rc)
@@ -387,7 +394,9 @@ class Arm:
             self.check(L.lo_reorder_device(ctx.h, xyz_dev or self.xyz_dev, self.n, cfg["curve"], 21, C.byref(coded)))
             tree = C.c_void_p()
             self.check(L.lo_octree_build(ctx.h, coded, cfg["n_max"], C.byref(tree)))
-        if self.world > 1 and not self.replicate:
+        if self.comm is not None:
+            coded, tree = self.comm.broadcast_structure(coded, tree, root=0)
+        elif self.world > 1 and not self.replicate:
             torch = self.torch
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -403,6 +412,10 @@ class Arm:
         self.L.lo_coded_destroy(coded)
 
     def radius(self, coded, tree, r, fingerprint=1):
+        if self.comm is not None:
+            csr, _, _, total = self.comm.radius(tree, coded, r, fingerprint=fingerprint)
+            self.global_totals[r] = total
+            return csr
         csr = C.c_void_p()
         self.check(self.L.lo_radius_range(self.ctx.h, tree, coded, 1, 0, r, self.b0, self.b1, fingerprint,
                                           C.byref(csr)))
@@ -452,7 +465,7 @@ class Arm:
         for _ in range(reps):
             t0 = time.perf_counter()
             coded, tree = self.build_structure()
-            if self.world > 1 and not self.replicate:
+            if self.world > 1 and not self.replicate and self.comm is None:
                 acc.setdefault("broadcast", []).append(self.bcast_last_ms)
             for name, t in ctx.stage_times():
                 acc.setdefault(name, []).append(t)
@@ -474,8 +487,11 @@ class Arm:
         coded, tree = self.build_structure()
         for k in self.cfg["ks"]:
             def one():
-                res = C.c_void_p()
-                self.check(self.L.lo_knn_range(self.ctx.h, tree, coded, k, self.b0, self.b1, 1, C.byref(res)))
+                if self.comm is not None:
+                    res, _ = self.comm.knn(tree, coded, k)
+                else:
+                    res = C.c_void_p()
+                    self.check(self.L.lo_knn_range(self.ctx.h, tree, coded, k, self.b0, self.b1, 1, C.byref(res)))
                 self.L.lo_knn_destroy(res)
             one()  # warm
             kms = self.timed(one, reps)
@@ -545,7 +561,9 @@ class Arm:
                 coded, tree = self.build_structure(dev_in[cur] if self.builds else None)
                 results = []
                 for key in keys:
-                    if mode == "knn":
+                    if mode == "knn" and self.comm is not None:
+                        res, _ = self.comm.knn(tree, coded, key)
+                    elif mode == "knn":
                         res = C.c_void_p()
                         self.check(L.lo_knn_range(ctx.h, tree, coded, key, self.b0, self.b1, 1, C.byref(res)))
                     else:
@@ -618,7 +636,9 @@ def run_ours(args, cfg):
     ms, launches, clocks = arm.main_region(args.steps, args.warmup)
     value = len(radii) * n / (ms * 1e-3)
     nbrs = sum(arm.totals.values())
-    if world > 1:
+    if arm.comm is not None:
+        nbrs = sum(arm.global_totals.values())
+    elif world > 1:
         _, nbrs = arm.D.global_row_base(nbrs, device=f"cuda:{local}")
     stages = arm.stages(max(2, min(args.steps, 4)))
     tinfo = arm.tinfo

@@ -36,7 +36,8 @@ typedef enum {
     LO_OUT_OF_MEMORY = 4,
     LO_CUDA_ERROR = 5,
     LO_NO_DEVICE = 6,
-    LO_RUNTIME_ERROR = 7  /* std::runtime_error: unreadable / malformed files (io.cpp, linear_octree.cpp:163-189) */
+    LO_RUNTIME_ERROR = 7, /* std::runtime_error: unreadable / malformed files (io.cpp, linear_octree.cpp:163-189) */
+    LO_NCCL_ERROR = 8     /* NCCL missing or a collective failed (multi-GPU entry points) */
 } lo_status;
 
 /* enum class Curve {Morton, Hilbert} (sfc.hpp:17) */
@@ -200,6 +201,17 @@ int lo_coded_write_pcb(lo_context* ctx, const lo_coded* coded, const char* path)
 int lo_octree_from_leaves(lo_context* ctx, const lo_coded* coded, const uint64_t* boundaries_host,
                           const uint32_t* offsets_host, uint64_t count, const double disc_box[6],
                           int level, int curve, uint32_t n_max, lo_octree** out);
+/* The internal-node link of LinearOctree(LeafArray, Discretizer, Curve, n_max)
+ * (linear_octree.cpp:84-137) without a cloud: validates the leaf array like the reference and
+ * links it on the device; *internal and *root are always set, nodes_host (cap entries) is written
+ * when it is large enough.  Searching needs lo_octree_from_leaves with the cloud it indexes. */
+int lo_link_leaves(lo_context* ctx, const uint64_t* boundaries_host, const uint32_t* offsets_host, uint64_t count,
+                   const double disc_box[6], int level, uint64_t* internal, int32_t* root,
+                   lo_internal_node* nodes_host, uint64_t cap);
+/* Discretizer::octant_bounds (sfc.cpp:110-127): the depth-`depth` octant (hx, hy, hz) of the
+ * discretizer box, padded outward by 2 ulps per side; out = {min xyz, max xyz}. */
+int lo_octant_bounds(const double disc_box[6], int level, uint32_t hx, uint32_t hy, uint32_t hz, int depth,
+                     double out[6]);
 /* LinearOctree::serialize / deserialize as LOC1 files. */
 int lo_octree_save(lo_context* ctx, const lo_octree* tree, const char* path);
 int lo_octree_load(lo_context* ctx, const lo_coded* coded, const char* path, lo_octree** out);
@@ -284,6 +296,41 @@ int lo_locality_log2(lo_context* ctx, const lo_knn_result* res, const lo_coded* 
 int lo_locality_histogram(lo_context* ctx, const lo_knn_result* res, const lo_coded* coded,
                           const uint32_t* centres_host, const uint32_t* index_map_host,
                           uint64_t* nbins, uint32_t* d_host, uint64_t* count_host, uint64_t cap);
+
+/* ---- multi-GPU (replaces the OpenMP loop over centres, search.cpp:297) ---- */
+/* One process per GPU; each process's context gets an NCCL communicator.  The structure is
+ * built once (on `root`) and broadcast; every rank searches its contiguous SFC slice of the
+ * centres, [n*rank/G, n*(rank+1)/G); each rank's CSR rows are global rows of the batch and are
+ * concatenated by offset (row_base = neighbours of the lower ranks).  Results are identical for
+ * any G.  NCCL (libnccl.so.2) is loaded on first use; LO_NCCL_ERROR when it is absent. */
+typedef struct lo_comm lo_comm;
+#define LO_COMM_ID_BYTES 128
+/* ncclGetUniqueId on one rank; the caller ships the 128 bytes to the others (any transport). */
+int lo_comm_unique_id(void* id_out);
+int lo_comm_init(lo_context* ctx, const void* id, int nranks, int rank, lo_comm** out);
+int lo_comm_info(const lo_comm* comm, int* rank, int* nranks);
+int lo_comm_destroy(lo_comm* comm);
+/* The rank's contiguous slice of n centres (host arithmetic). */
+int lo_shard_range(uint64_t n, int rank, int nranks, uint64_t* begin, uint64_t* end);
+/* Broadcast (CodedCloud, LinearOctree) from `root`: the root passes its handles (outputs set to
+ * NULL; it keeps computing while the broadcast runs on the communicator's stream, and destroying
+ * its handles waits for it); the others pass NULL and receive new handles on their context (FP32
+ * filter copies are rebuilt locally, not sent).  Timed as the stage "broadcast". */
+int lo_broadcast_structure(lo_comm* comm, const lo_coded* coded, const lo_octree* tree, int root,
+                           lo_coded** coded_out, lo_octree** tree_out);
+/* Single-process replication onto another context / device (cudaMemcpyPeerAsync; the same device
+ * works too): new handles on `dst`. */
+int lo_structure_copy(lo_context* dst, const lo_coded* coded, const lo_octree* tree, lo_coded** coded_out,
+                      lo_octree** tree_out);
+/* run_radius_batch in Full mode over this rank's slice: *out holds rows [row_begin, row_begin +
+ * rows) with local offsets; global offset = local + *row_base; *total = neighbours of all ranks
+ * (one NCCL all-gather of u64 totals). */
+int lo_radius_sharded(lo_comm* comm, const lo_octree* tree, const lo_coded* coded, int method, int shape,
+                      double radius, int fingerprint, lo_csr** out, uint64_t* row_begin, uint64_t* row_base,
+                      uint64_t* total);
+/* run_knn_batch in Full mode over this rank's slice (fixed-width rows: no exchange). */
+int lo_knn_sharded(lo_comm* comm, const lo_octree* tree, const lo_coded* coded, uint32_t k, int fingerprint,
+                   lo_knn_result** out, uint64_t* row_begin);
 
 /* ---- synthetic clouds (host; io.cpp:122-130 and SURVEY.md §8d) ---------------------- */
 int lo_generate_uniform(uint64_t n, uint64_t seed, double extent, double* xyz_host);

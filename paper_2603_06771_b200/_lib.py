@@ -16,7 +16,7 @@ P = C.c_void_p
 PP = C.POINTER(C.c_void_p)
 u32, u64, i32, f64, cint = C.c_uint32, C.c_uint64, C.c_int32, C.c_double, C.c_int
 
-OK, INVALID_ARGUMENT, DOMAIN_ERROR, LOGIC_ERROR, OUT_OF_MEMORY, CUDA_ERROR, NO_DEVICE, RUNTIME_ERROR = range(8)
+OK, INVALID_ARGUMENT, DOMAIN_ERROR, LOGIC_ERROR, OUT_OF_MEMORY, CUDA_ERROR, NO_DEVICE, RUNTIME_ERROR, NCCL_ERROR = range(9)
 
 
 class CodedInfo(C.Structure):
@@ -98,6 +98,17 @@ SIGNATURES = {
     "lo_knn_info_get": (cint, [P, P, P, P]),
     "lo_knn_download": (cint, [P, P, P, P, P]),
     "lo_knn_download_async": (cint, [P, P, P, P, P]),
+    "lo_link_leaves": (cint, [P, P, P, u64, P, cint, P, P, P, u64]),
+    "lo_comm_unique_id": (cint, [P]),
+    "lo_comm_init": (cint, [P, P, cint, cint, PP]),
+    "lo_comm_info": (cint, [P, P, P]),
+    "lo_comm_destroy": (cint, [P]),
+    "lo_shard_range": (cint, [u64, cint, cint, P, P]),
+    "lo_broadcast_structure": (cint, [P, P, P, cint, PP, PP]),
+    "lo_structure_copy": (cint, [P, P, P, PP, PP]),
+    "lo_radius_sharded": (cint, [P, P, P, cint, cint, f64, cint, PP, P, P, P]),
+    "lo_knn_sharded": (cint, [P, P, P, u32, cint, PP, P]),
+    "lo_octant_bounds": (cint, [P, cint, u32, u32, u32, cint, P]),
     "lo_knn_destroy": (cint, [P]),
     "lo_locality_log2": (cint, [P, P, P, P, cint, P]),
     "lo_generate_uniform": (cint, [u64, u64, f64, P]),
@@ -158,8 +169,12 @@ class FileFormatError(LinoctError, RuntimeError):
     """std::runtime_error: unreadable or malformed PCB1 / XYZ / LOC1 files"""
 
 
+class NcclError(LinoctError, RuntimeError):
+    """NCCL missing or a collective failed (multi-GPU entry points)"""
+
+
 _EXC = {INVALID_ARGUMENT: InvalidArgument, DOMAIN_ERROR: DomainError, LOGIC_ERROR: LogicError,
-        RUNTIME_ERROR: FileFormatError}
+        RUNTIME_ERROR: FileFormatError, NCCL_ERROR: NcclError}
 
 
 def check(status: int) -> None:

@@ -16,7 +16,7 @@ OBJ = os.path.join(os.environ.get("LO_BUILD_DIR", HERE), "_build")
 LIB = os.path.join(os.environ.get("LO_BUILD_DIR", HERE), "liblinoct_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CUDA_SOURCES = ["context.cu", "reorder.cu", "octree.cu", "radius.cu", "radius_struct.cu", "knn.cu", "io.cu", "centres.cu"]
+CUDA_SOURCES = ["context.cu", "reorder.cu", "octree.cu", "radius.cu", "radius_struct.cu", "knn.cu", "io.cu", "centres.cu", "comm.cu"]
 CXX_SOURCES = ["gen.cpp"]
 
 # -fmad=false: no DFMA contraction anywhere, the FP64 predicates must be the reference's

@@ -200,6 +200,7 @@ static void resolve_stages(lo_context* ctx) {
     sync(ctx);
     for (auto& s : ctx->stages) {
         float ms = 0.f;
+        cudaEventSynchronize(s.b);  // stages may be timed on another stream (broadcast)
         cudaEventElapsedTime(&ms, s.a, s.b);
         ctx->stage_ms.emplace_back(s.name, ms);
         cudaEventDestroy(s.a);

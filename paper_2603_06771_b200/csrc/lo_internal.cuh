@@ -185,6 +185,7 @@ struct lo_coded {
     float4* pf = nullptr;
     double origin[3] = {};
     double bmax = 0.0;  // >= |p - origin| on every axis (the cube side)
+    cudaEvent_t reader = nullptr;  // another stream (broadcast / peer copy) reads the buffers
 };
 
 struct lo_octree {
@@ -204,6 +205,7 @@ struct lo_octree {
     double* rb = nullptr;               // [tnodes*6] padded octant boxes (Struct; built lazily)
     float4* rbf = nullptr;              // [tnodes*2] the same, FP32 outward-rounded, relative to origin
     int max_depth = 0;
+    cudaEvent_t reader = nullptr;       // another stream (broadcast / peer copy) reads the buffers
 };
 
 namespace lo {

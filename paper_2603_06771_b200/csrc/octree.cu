@@ -634,15 +634,14 @@ __global__ void leaf_link(const u64* __restrict__ b, const u32* __restrict__ off
     }
 }
 
-lo_octree* octree_from_leaves(lo_context* ctx, const lo_coded* coded, const u64* b_host,
-                              const u32* off_host, u64 count, const double disc_box[6], int level,
-                              int curve, u32 n_max) {
-    require(coded != nullptr, LO_INVALID_ARGUMENT, "null coded cloud");
+// LinearOctree(LeafArray, ...) validation (linear_octree.cpp:88-103) and the device link of the
+// internal nodes from the leaves alone (no cloud needed).
+static LeafBuild link_leaf_array(lo_context* ctx, const u64* b_host, const u32* off_host, u64 count,
+                                 const double disc_box[6], int level) {
     // Discretizer ctor (sfc.cpp:99-104)
     require(level >= 0 && level <= kMaxLevel, LO_INVALID_ARGUMENT, "level out of range");
     require(disc_box[0] <= disc_box[3] && disc_box[1] <= disc_box[4] && disc_box[2] <= disc_box[5],
             LO_INVALID_ARGUMENT, "inverted bounding box");
-    // LinearOctree(LeafArray, ...) validation (linear_octree.cpp:88-103)
     const u64 full = 1ull << (3 * level);
     require(count >= 2 && b_host[0] == 0 && b_host[count - 1] == full && off_host[0] == 0,
             LO_INVALID_ARGUMENT, "linear octree: malformed leaf array");
@@ -653,11 +652,7 @@ lo_octree* octree_from_leaves(lo_context* ctx, const lo_coded* coded, const u64*
         if (!aligned_pow8 || off_host[i] > off_host[i + 1])
             throw Error(LO_INVALID_ARGUMENT, "linear octree: misaligned leaf span at " + std::to_string(i));
     }
-    // the device tree searches this cloud: its leaves must index exactly its points
-    require(off_host[count - 1] == coded->n && level == coded->level && curve == coded->curve,
-            LO_INVALID_ARGUMENT, "linear octree: leaf array does not match the coded cloud");
     const u64 L = count - 1;
-    stage_begin(ctx, "build");
     LeafBuild lb;
     lb.leaves = L;
     lb.bounds = dalloc_t<u64>(ctx, count);
@@ -680,9 +675,47 @@ lo_octree* octree_from_leaves(lo_context* ctx, const lo_coded* coded, const u64*
     }
     dfree(ctx, cnt);
     dfree(ctx, S);
+    return lb;
+}
+
+static void free_leaf_build(lo_context* ctx, LeafBuild& lb) {
+    dfree(ctx, lb.bounds), dfree(ctx, lb.offsets), dfree(ctx, lb.nodes), dfree(ctx, lb.nchild);
+    lb = LeafBuild{};
+}
+
+lo_octree* octree_from_leaves(lo_context* ctx, const lo_coded* coded, const u64* b_host,
+                              const u32* off_host, u64 count, const double disc_box[6], int level,
+                              int curve, u32 n_max) {
+    require(coded != nullptr, LO_INVALID_ARGUMENT, "null coded cloud");
+    stage_begin(ctx, "build");
+    LeafBuild lb = link_leaf_array(ctx, b_host, off_host, count, disc_box, level);
+    // the device tree searches this cloud: its leaves must index exactly its points
+    if (!(off_host[count - 1] == coded->n && level == coded->level && curve == coded->curve)) {
+        free_leaf_build(ctx, lb);
+        throw Error(LO_INVALID_ARGUMENT, "linear octree: leaf array does not match the coded cloud");
+    }
     lo_octree* t = finish_octree(ctx, coded, lb, n_max, level, curve, disc_box);
     stage_end(ctx);
     return t;
+}
+
+// Discretizer::octant_bounds (sfc.cpp:110-127) on the host: one padded box.
+static void octant_bounds_host(const double box[6], int level, u32 hx, u32 hy, u32 hz, int depth, double out[6]) {
+    require(level >= 0 && level <= kMaxLevel && depth >= 0 && depth <= level, LO_INVALID_ARGUMENT,
+            "depth out of range");
+    if (depth == 0) {
+        std::memcpy(out, box, 6 * sizeof(double));
+        return;
+    }
+    const double inv = std::ldexp(1.0, -depth);
+    const u32 h[3] = {hx, hy, hz};
+    for (int a = 0; a < 3; ++a) {
+        const double side = (box[3 + a] - box[a]) * inv;
+        const double lo = box[a] + h[a] * side;
+        const double hi = lo + side;
+        out[a] = dbl_from_order_key(dbl_order_key(lo) - 2);
+        out[3 + a] = dbl_from_order_key(dbl_order_key(hi) + 2);
+    }
 }
 
 }  // namespace lo
@@ -760,6 +793,31 @@ int lo_octree_download(lo_context* ctx, const lo_octree* t, uint64_t* boundaries
     });
 }
 
+int lo_link_leaves(lo_context* ctx, const uint64_t* boundaries_host, const uint32_t* offsets_host, uint64_t count,
+                   const double disc_box[6], int level, uint64_t* internal, int32_t* root,
+                   lo_internal_node* nodes_host, uint64_t cap) {
+    return api_ctx(ctx, [&] {
+        require(boundaries_host && offsets_host && disc_box && internal && root, LO_INVALID_ARGUMENT,
+                "null argument");
+        LeafBuild lb = link_leaf_array(ctx, boundaries_host, offsets_host, count, disc_box, level);
+        *internal = lb.internal;
+        *root = lb.internal > 0 ? 0 : ~0;
+        if (nodes_host && lb.internal && cap >= lb.internal)
+            LO_CUDA(cudaMemcpyAsync(nodes_host, lb.nodes, sizeof(lo_internal_node) * lb.internal,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        sync(ctx);
+        free_leaf_build(ctx, lb);
+    });
+}
+
+int lo_octant_bounds(const double disc_box[6], int level, uint32_t hx, uint32_t hy, uint32_t hz, int depth,
+                     double out[6]) {
+    return api([&] {
+        require(disc_box && out, LO_INVALID_ARGUMENT, "null argument");
+        octant_bounds_host(disc_box, level, hx, hy, hz, depth, out);
+    });
+}
+
 int lo_octree_node_bounds(lo_context* ctx, const lo_octree* t, const int32_t* refs_host,
                           uint64_t count, double* boxes_host) {
     return api_ctx(ctx, [&] {
@@ -832,6 +890,10 @@ int lo_octree_destroy(lo_octree* t) {
     if (!t) return LO_OK;
     return api_ctx(t->ctx, [&] {
         lo_context* ctx = t->ctx;
+        if (t->reader) {  // a broadcast / peer copy may still read the buffers: free behind it
+            LO_CUDA(cudaStreamWaitEvent(ctx->stream, t->reader, 0));
+            cudaEventDestroy(t->reader);
+        }
         dfree(ctx, t->bounds);
         dfree(ctx, t->offsets);
         dfree(ctx, t->nodes);

@@ -746,6 +746,10 @@ int lo_coded_destroy(lo_coded* c) {
     if (!c) return LO_OK;
     return api_ctx(c->ctx, [&] {
         lo_context* ctx = c->ctx;
+        if (c->reader) {  // a broadcast / peer copy may still read the buffers: free behind it
+            LO_CUDA(cudaStreamWaitEvent(ctx->stream, c->reader, 0));
+            cudaEventDestroy(c->reader);
+        }
         dfree(ctx, c->x);
         dfree(ctx, c->y);
         dfree(ctx, c->z);

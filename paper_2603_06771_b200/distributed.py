@@ -122,3 +122,69 @@ def broadcast_structure(ctx, coded_h, tree_h, src: int = 0, group=None):
     broadcast_buffers(views, src=src, group=group)
     torch.cuda.synchronize(ctx.device)
     return coded_h, tree_h, ci, ti
+
+
+# ---- the C-ABI path: the library's own NCCL communicator (lo_comm) ---------------------------
+class Comm:
+    """lo_comm (include/linoct_b200.h, csrc/comm.cu): an NCCL communicator owned by the library on
+    one context.  torch.distributed only ships the 128-byte NCCL unique id (any process group,
+    gloo included); the structure broadcast, the per-rank totals all-gather and the sharded
+    searches are C-ABI calls a C++ caller makes the same way."""
+
+    def __init__(self, ctx, rank: int, world: int, group=None, uid: bytes | None = None):
+        L = _lib.lib()
+        if uid is None:
+            box = [None]
+            if rank == 0:
+                buf = C.create_string_buffer(128)
+                check(L.lo_comm_unique_id(buf))
+                box = [buf.raw]
+            if world > 1:
+                dist.broadcast_object_list(box, src=0, group=group)
+            uid = box[0]
+        h = C.c_void_p()
+        check(L.lo_comm_init(ctx.h, C.create_string_buffer(uid, 128), world, rank, C.byref(h)))
+        self.h, self.ctx, self.rank, self.world = h, ctx, rank, world
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.lib().lo_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def shard(self, n: int) -> tuple[int, int]:
+        b, e = C.c_uint64(), C.c_uint64()
+        check(_lib.lib().lo_shard_range(n, self.rank, self.world, C.byref(b), C.byref(e)))
+        return b.value, e.value
+
+    def broadcast_structure(self, coded_h, tree_h, root: int = 0):
+        """Root passes its handles and gets them back; the others get new handles."""
+        c, t = C.c_void_p(), C.c_void_p()
+        check(_lib.lib().lo_broadcast_structure(self.h, coded_h, tree_h, root, C.byref(c), C.byref(t)))
+        return (coded_h, tree_h) if self.rank == root else (c, t)
+
+    def radius(self, tree_h, coded_h, r: float, method: int = 1, shape: int = 0, fingerprint: int = 1):
+        """-> (csr handle, row_begin, row_base, total neighbours of all ranks)"""
+        csr = C.c_void_p()
+        b, base, tot = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(_lib.lib().lo_radius_sharded(self.h, tree_h, coded_h, method, shape, r, fingerprint, C.byref(csr),
+                                           C.byref(b), C.byref(base), C.byref(tot)))
+        return csr, b.value, base.value, tot.value
+
+    def knn(self, tree_h, coded_h, k: int, fingerprint: int = 1):
+        res = C.c_void_p()
+        b = C.c_uint64()
+        check(_lib.lib().lo_knn_sharded(self.h, tree_h, coded_h, k, fingerprint, C.byref(res), C.byref(b)))
+        return res, b.value
+
+
+def structure_copy(dst_ctx, coded_h, tree_h):
+    """lo_structure_copy: single-process replication onto another context (peer copies)."""
+    c, t = C.c_void_p(), C.c_void_p()
+    check(_lib.lib().lo_structure_copy(dst_ctx.h, coded_h, tree_h, C.byref(c), C.byref(t)))
+    return c, t

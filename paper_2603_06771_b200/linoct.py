@@ -86,9 +86,11 @@ class Context:
         self.device = device
 
     def close(self):
+        """Destroys the context; a no-op while handles created on it are still alive (the C ABI
+        refuses with LO_LOGIC_ERROR), retried when this object is collected."""
         if getattr(self, "h", None):
-            _lib.lib().lo_context_destroy(self.h)
-            self.h = None
+            if _lib.lib().lo_context_destroy(self.h) == _lib.OK:
+                self.h = None
 
     def __del__(self):
         try:

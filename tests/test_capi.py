@@ -51,3 +51,42 @@ def test_host_argument_errors_before_device():
         linoct.SearchKernel(linoct.KernelShape.Sphere, (0, 0, 0), -1.0)
     with pytest.raises(linoct.InvalidArgument):
         linoct.PointCloud(np.array([[0.0, np.nan, 1.0]]))
+
+
+def test_octant_bounds_host_matches_reference(ref):
+    """lo_octant_bounds (Discretizer::octant_bounds, sfc.cpp:110-127) is host arithmetic in the library:
+    bit-equal to the reference's padded boxes on random octants of random boxes."""
+    L = _lib.lib()
+    rng = np.random.default_rng(3)
+    for _ in range(300):
+        lo_ = rng.uniform(-1e3, 1e3, 3)
+        box = np.concatenate([lo_, lo_ + rng.uniform(0, 500, 3)])
+        level = int(rng.integers(1, 22))
+        depth = int(rng.integers(0, level + 1))
+        h = rng.integers(0, 2 ** depth, 3) if depth else np.zeros(3, np.int64)
+        out = np.zeros(6)
+        assert L.lo_octant_bounds(box.ctypes.data_as(C.c_void_p), level, int(h[0]), int(h[1]), int(h[2]), depth,
+                                  out.ctypes.data_as(C.c_void_p)) == _lib.OK
+        want = ref.octant_bounds(box, int(h[0]), int(h[1]), int(h[2]), depth, level)
+        assert np.array_equal(out.view(np.uint64), np.asarray(want, np.float64).view(np.uint64))
+    out = np.zeros(6)
+    assert L.lo_octant_bounds(box.ctypes.data_as(C.c_void_p), 3, 0, 0, 0, 4, out.ctypes.data_as(C.c_void_p)) == \
+        _lib.INVALID_ARGUMENT
+
+
+def test_shard_range_host():
+    """lo_shard_range (host arithmetic): contiguous, covering, balanced slices = distributed.shard_range."""
+    from paper_2603_06771_b200 import distributed as D
+    L = _lib.lib()
+    for n in (0, 1, 7, 1000, 100_000_000, 2 ** 32 - 1):
+        for g in (1, 2, 3, 8):
+            prev = 0
+            for r in range(g):
+                b, e = C.c_uint64(), C.c_uint64()
+                assert L.lo_shard_range(n, r, g, C.byref(b), C.byref(e)) == _lib.OK
+                assert (b.value, e.value) == D.shard_range(n, r, g)
+                assert b.value == prev and e.value - b.value in (n // g, n // g + 1)
+                prev = e.value
+            assert prev == n
+    b, e = C.c_uint64(), C.c_uint64()
+    assert L.lo_shard_range(10, 2, 2, C.byref(b), C.byref(e)) == _lib.INVALID_ARGUMENT
