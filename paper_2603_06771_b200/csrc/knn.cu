@@ -110,6 +110,7 @@ constexpr int kKnnSmemBudget = 200 * 1024;
 }  // namespace lo
 
 #include "knn_float.cuh"
+#include "knn_warp.cuh"
 
 namespace lo {
 
@@ -404,7 +405,31 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
         const int blocks = static_cast<int>(std::max<u64>(
             1, std::min<u64>((tiles + warps - 1) / warps, static_cast<u64>(ctx->sm_count) * per_sm)));
         stage_begin(ctx, "knn");
-        if (q.m && use_float) {
+        // k <= 64: the warp-cooperative kernel (knn_warp.cuh); LO_KNN_LEGACY=1 keeps the per-lane heaps
+        const bool warp_kernel = use_float && kh <= 64 && !env_flag("LO_KNN_LEGACY");
+        if (q.m && warp_kernel) {
+            float E = static_cast<float>(std::ldexp(std::max(c->bmax, q.bmax), -23));
+            E = std::nextafter(E, INFINITY);  // round up
+            const u32 seed_half = std::max<u32>(16, kh);
+            const size_t per_warp = knn_warp_smem_per_warp(kh);
+            const size_t wsmem = kKwWarps * per_warp;
+            const int wper_sm = std::max(1, std::min(16, static_cast<int>(224 * 1024 / wsmem)));
+            const int wblocks = static_cast<int>(std::max<u64>(
+                1, std::min<u64>((tiles + kKwWarps - 1) / kKwWarps, static_cast<u64>(ctx->sm_count) * wper_sm)));
+            u64* counter = dalloc_t<u64>(ctx, 1);
+            LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
+            if (kh <= 32) {
+                ensure_smem_attr(ctx, kAttrKnnW1, knn_warp_kernel<1>, kKwWarps * knn_warp_smem_per_warp(32));
+                knn_warp_kernel<1><<<wblocks, 32 * kKwWarps, wsmem, ctx->stream>>>(
+                    t->tf, c->x, c->y, c->z, c->n, q, seed_base, seed_half, E, kh, out->idx, out->dist, counter);
+            } else {
+                ensure_smem_attr(ctx, kAttrKnnW2, knn_warp_kernel<2>, kKwWarps * knn_warp_smem_per_warp(64));
+                knn_warp_kernel<2><<<wblocks, 32 * kKwWarps, wsmem, ctx->stream>>>(
+                    t->tf, c->x, c->y, c->z, c->n, q, seed_base, seed_half, E, kh, out->idx, out->dist, counter);
+            }
+            LO_CHECK_LAUNCH();
+            dfree(ctx, counter);
+        } else if (q.m && use_float) {
             float E = static_cast<float>(std::ldexp(std::max(c->bmax, q.bmax), -23));
             E = std::nextafter(E, INFINITY);  // round up
             const u32 seed_half = std::max<u32>(16, kh);

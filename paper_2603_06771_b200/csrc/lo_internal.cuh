@@ -464,7 +464,7 @@ int api_ctx(lo_context* ctx, F&& f) {
 }
 
 // Raises a kernel's dynamic shared-memory limit once per context (= per device).
-enum : unsigned { kAttrSort = 1u, kAttrReplay = 2u };
+enum : unsigned { kAttrSort = 1u, kAttrReplay = 2u, kAttrKnnW1 = 4u, kAttrKnnW2 = 8u };
 template <class K>
 void ensure_smem_attr(lo_context* ctx, unsigned bit, K kernel, size_t smem) {
     if (ctx->smem_attrs & bit) return;

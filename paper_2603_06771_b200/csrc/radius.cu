@@ -135,10 +135,12 @@ static bool float_path(const lo_octree* t, const lo_coded* c, const Queries& q, 
 }
 
 
+// fps != nullptr (count pass on the FP32 path): the row digests are computed by the count
+// kernel itself (radius_pt_kernel<..., DIGEST>); returns whether it did.
 template <bool FILL>
-static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const lo_coded* c,
+static bool launch_radius(lo_context* ctx, int shape, const lo_octree* t, const lo_coded* c,
                           const Queries& q, double r, u32* counts, const u64* offsets, u32* out,
-                          const RecArgs& ra = RecArgs{}) {
+                          const RecArgs& ra = RecArgs{}, u64* fps = nullptr) {
     const double r2 = r * r;  // SearchKernel ctor (geometry.hpp:107)
     const u64 tiles = ra.list ? ra.list_n : (q.m + 31) / 32;
     const int blocks = static_cast<int>(std::max<u64>(1, std::min<u64>((tiles + kRadiusWarps - 1) / kRadiusWarps,
@@ -165,11 +167,21 @@ static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
         LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
         const int pblocks = static_cast<int>(std::max<u64>(
             1, std::min<u64>((tiles + kPtWarps - 1) / kPtWarps, static_cast<u64>(ctx->sm_count) * 8)));
+        const int digest = FILL || !fps ? 0 : (c->n <= (1u << 24) ? 2 : 1);
 #define LO_RADIUS_F(S)                                                                          \
     case S:                                                                                     \
-        radius_pt_kernel<S, FILL><<<pblocks, kPtThreads, 0, ctx->stream>>>(                    \
-            t->tf, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, counts, offsets, out,        \
-            counter, ra.rp, ra.list, ra.list_n);                                                \
+        if (digest == 2)                                                                        \
+            radius_pt_kernel<S, FILL, 2><<<pblocks, kPtThreads, 0, ctx->stream>>>(              \
+                t->tf, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, counts, offsets, out,    \
+                counter, ra.rp, ra.list, ra.list_n, fps);                                       \
+        else if (digest == 1)                                                                   \
+            radius_pt_kernel<S, FILL, 1><<<pblocks, kPtThreads, 0, ctx->stream>>>(              \
+                t->tf, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, counts, offsets, out,    \
+                counter, ra.rp, ra.list, ra.list_n, fps);                                       \
+        else                                                                                    \
+            radius_pt_kernel<S, FILL, 0><<<pblocks, kPtThreads, 0, ctx->stream>>>(              \
+                t->tf, c->pf, c->x, c->y, c->z, q, ft, compact, r, r2, counts, offsets, out,    \
+                counter, ra.rp, ra.list, ra.list_n, nullptr);                                   \
         break;
         switch (shape) {
             LO_RADIUS_F(LO_SPHERE)
@@ -181,7 +193,7 @@ static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
 #undef LO_RADIUS_F
         LO_CHECK_LAUNCH();
         dfree(ctx, counter);
-        return;
+        return digest != 0;
     }
     require(ra.list == nullptr, LO_LOGIC_ERROR, "tile-list fill needs the FP32 path");
 #define LO_RADIUS_CASE(S)                                                                        \
@@ -199,6 +211,7 @@ static void launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
     }
 #undef LO_RADIUS_CASE
     LO_CHECK_LAUNCH();
+    return false;
 }
 
 
@@ -235,8 +248,15 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
                 ovf = ovf_n = nullptr;
             }
         }
+        // LO_DIGEST_FUSED=1: the row digests ride along the count pass (radius_pt_kernel<..., DIGEST>).
+        // Off by default: hashing each buffer's members per lane diverges with the members per row
+        // (cfg3 count 40.4 -> 62.5 ms, cfg1 r = 3 5.1 -> 10.4 ms) and costs more than the separate
+        // radius_digest pass it saves (9.2 ms at cfg3).
+        if (fingerprint) out->fps = big_alloc_t<u64>(ctx, q.m, &out->cap[1]);
+        u64* fused_fps = fingerprint && env_flag("LO_DIGEST_FUSED") ? out->fps : nullptr;
         stage_begin(ctx, "radius_count");
-        if (q.m) launch_radius<false>(ctx, shape, t, c, q, r, out->counts, nullptr, nullptr, ra);
+        bool digested = false;
+        if (q.m) digested = launch_radius<false>(ctx, shape, t, c, q, r, out->counts, nullptr, nullptr, ra, fused_fps);
         stage_end(ctx);
         stage_begin(ctx, "radius_scan");
         exclusive_scan_u32_to_u64(ctx, out->counts, out->offsets, q.m);
@@ -264,8 +284,7 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
         ra = RecArgs{};
         ovf = ovf_n = nullptr;
         LO_CUDA(cudaEventRecord(e1, ctx->stream));
-        if (fingerprint) {
-            out->fps = big_alloc_t<u64>(ctx, q.m, &out->cap[1]);
+        if (fingerprint && !digested) {
             // LO_DIGEST_AUX=1: the digests trail on the aux stream, overlapping the caller's next
             // batch.  Off by default: with the count kernels issue-bound, the overlap cost more than
             // it hid (cfg1 e2e 28.6 ms with it, 28.2 ms inline).

@@ -29,8 +29,10 @@ struct PtShared {
     u32 stack[kStackCap];
     float4 buf[32];      // candidate (x, y, z) relative FP32, .w = point index bits
     u32 bix[32];         // candidate point indices, staged per leaf (loaded per buffer)
-    float4 qf[32];       // queries, FP32
-    __align__(16) float qx[32];  // queries, FP32 SoA: (q[2p], q[2p+1]) loads as one f32x2
+    float4 qf[32];       // queries, FP32 relative to the cloud origin (walk: node-box tests)
+    // queries, FP32 relative to the tile origin (point tests), SoA: (q[2p], q[2p+1]) loads as
+    // one f32x2
+    __align__(16) float qx[32];
     __align__(16) float qy[32];
     __align__(16) float qz[32];
     double qd[32][3];    // queries, FP64 (band decisions)
@@ -133,8 +135,8 @@ __device__ __forceinline__ void process_buffer(PtShared& S, const float4 P, u32 
             }
             unpack2(d2, v0, v1);
         } else {
-            v0 = metric_f<SHAPE>(S.qf[b], P);
-            v1 = metric_f<SHAPE>(S.qf[b + 1], P);
+            v0 = metric_f<SHAPE>(make_float4(S.qx[b], S.qy[b], S.qz[b], 0.f), P);
+            v1 = metric_f<SHAPE>(make_float4(S.qx[b + 1], S.qy[b + 1], S.qz[b + 1], 0.f), P);
         }
         u32 in0 = __ballot_sync(~0u, v0 < lo_thr);
         u32 in1 = __ballot_sync(~0u, v1 < lo_thr);
@@ -489,21 +491,61 @@ static inline u32 replay_records(lo_context* ctx, const RecSetup& rs, u64 m, con
     return read_scalar(ctx, rs.ovf_n);
 }
 
-template <int SHAPE, bool FILL>
+// Point tests relative to a tile origin.  The FP32 filter's error bound grows with the magnitude
+// of the FP32 coordinates (search_common.cuh: d = 2 * 2^-23 * B + 2^-23 * 2r, B >= |p - o|).
+// Relative to the cloud origin B is the cube side (~3 km at cfg3, d ~ 7e-4 at r = 1, so ~1 % of
+// the candidate pairs fell in the FP64 band); relative to the tile's first query, B only has to
+// bound |p - o_t| for candidates that can be near the threshold, i.e. within 2r of a tile query:
+// B = max_tile |q - o_t| + 2r, a few metres.  Farther candidates are outside whatever their
+// rounding: their FP32 difference keeps its relative error <= 2^-23 and exceeds 1.99 r on some
+// axis (d < 0.01 r).  Candidate and query coordinates are rounded from FP64 differences
+// fl32(fl64(p - o_t)), exactly the model of the bound.  A tile too wide for the test
+// (d >= 0.01 r) sends every candidate to the exact predicate (lo = 0, hi = +inf).
+struct TileTest {
+    float lo, hi;  // Sphere / Circle: squared-distance thresholds; Cube / Square: L-inf ones
+};
+template <int SHAPE>
+__device__ __forceinline__ TileTest tile_test(double r, double ext) {
+    const double u = 0x1p-23;
+    const double B = ext + 2.0 * r;
+    const double d = 2.0 * u * B + u * 2.0 * r;
+    const double r2 = r * r;
+    TileTest t;
+    if (!(d < 0.01 * r)) {
+        t.lo = 0.f;
+        t.hi = INFINITY;
+        return t;
+    }
+    if (SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE) {
+        const double M = 1.25 * (3.0 * u * 4.0 * r2 + 2.0 * 1.7320508075688772 * 2.0 * r * d + 3.0 * d * d +
+                                 0x1p-49 * 4.0 * r2);
+        t.lo = __double2float_rd(r2 - M);
+        t.hi = __double2float_ru(r2 + M);
+    } else {
+        const double ml = 1.25 * (d + 0x1p-50 * r);
+        t.lo = __double2float_rd(r - ml);
+        t.hi = __double2float_ru(r + ml);
+    }
+    return t;
+}
+
+// DIGEST (count pass only): the FNV-1a-64 row digests (search.cpp:263-271, :345-347) are folded in
+// as the members are found -- buffers follow the DFS code order and slots keep point order, so
+// lane L meets row L's members in ascending order, exactly the order the digest hashes them.
+// This replaces a separate pass that re-read every CSR row (25.5 GB at cfg3).  1: u32 indices,
+// 2: indices < 2^24 (five zero bytes fold into one multiply).
+template <int SHAPE, bool FILL, int DIGEST = 0>
 __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
     const TNodeF* __restrict__ tf, const float4* __restrict__ pf, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, Queries q, FloatTest ft,
     float compact, double r, double r2, u32* __restrict__ counts, const u64* __restrict__ offsets,
     u32* __restrict__ out, u64* tile_counter, RecPool rp, const u32* __restrict__ tile_list,
-    u64 list_n) {
+    u64 list_n, u64* __restrict__ fps) {
     __shared__ PtShared shared_s[kPtWarps];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     PtShared& S = shared_s[w];
     const u64 ntiles = tile_list ? list_n : (q.m + 31) / 32;
     const int cl = lane & 7, grp = lane >> 3;
-    constexpr bool kSq = SHAPE == LO_SPHERE || SHAPE == LO_CIRCLE;
-    const float lo_thr = kSq ? ft.t_lo : ft.r_lo;
-    const float hi_thr = kSq ? ft.t_hi : ft.r_hi;
     u64 chunk_base = 0;  // count pass: this warp's current record chunk (in records)
     u32 chunk_left = 0;
     for (;;) {
@@ -529,11 +571,23 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             load_query(q, qi, cx, cy, cz);
             qf = load_query_f(q, qi);
         }
+        // tile origin = the tile's first query (lane 0 is active in every tile)
+        const double ox = __shfl_sync(~0u, cx, 0), oy = __shfl_sync(~0u, cy, 0), oz = __shfl_sync(~0u, cz, 0);
+        float ext = 0.f;
         __syncwarp();
         S.qf[lane] = qf;
-        S.qx[lane] = qf.x;
-        S.qy[lane] = qf.y;
-        S.qz[lane] = qf.z;
+        if (active) {
+            S.qx[lane] = __double2float_rn(cx - ox);
+            S.qy[lane] = __double2float_rn(cy - oy);
+            S.qz[lane] = __double2float_rn(cz - oz);
+            ext = __double2float_ru(fmax(fmax(fabs(cx - ox), fabs(cy - oy)), fabs(cz - oz)));
+        } else {
+            S.qx[lane] = S.qy[lane] = S.qz[lane] = INFINITY;  // never near anything
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ext = fmaxf(ext, __shfl_xor_sync(~0u, ext, o));
+        const TileTest tt = tile_test<SHAPE>(r, static_cast<double>(ext));
+        const float lo_thr = tt.lo, hi_thr = tt.hi;
         S.qd[lane][0] = cx;
         S.qd[lane][1] = cy;
         S.qd[lane][2] = cz;
@@ -557,6 +611,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
         const bool gcompact = fmaxf(fmaxf(gh[0] - gl[0], gh[1] - gl[1]), gh[2] - gl[2]) <= compact;
         u32 fill = 0, qmask = 0;  // buffer occupancy and interested queries (warp-uniform)
         u32 nrec = 0;             // count pass: buffers recorded for the replay
+        u64 hash = kFnvOffset;    // DIGEST: row L's FNV-1a-64 so far
         u32* rec_tile = (!FILL && rp.pool && chunk_left >= rp.cap) ? rp.pool + chunk_base * 64 : nullptr;
         auto flush = [&]() {
             // the buffer's points are loaded here, all 32 at once (one latency per buffer instead
@@ -564,14 +619,20 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             float4 P = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
             if (static_cast<u32>(lane) < fill) {
                 const u32 g = S.bix[lane];
-                P = __ldg(pf + g);
-                P.w = __uint_as_float(g);
+                P = make_float4(__double2float_rn(__ldg(px + g) - ox), __double2float_rn(__ldg(py + g) - oy),
+                                __double2float_rn(__ldg(pz + g) - oz), __uint_as_float(g));
             }
             u32 mymask = 0;
             process_buffer<SHAPE, FILL>(S, P, fill, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2,
                                         out_tile, mine, mymask);
             if (!FILL) {
                 mine += __popc(mymask);
+                if (DIGEST) {
+                    for (u32 mm = mymask; mm; mm &= mm - 1) {
+                        const u32 g = S.bix[__ffs(mm) - 1];
+                        hash = DIGEST == 2 ? fnv_u24(hash, g) : fnv_u32(hash, g);
+                    }
+                }
                 // buffers without members leave no record (the replay would skip them anyway)
                 if (rec_tile && __any_sync(~0u, mymask != 0)) {
                     if (nrec < rp.cap) {
@@ -633,6 +694,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             flush();  // partial last buffer
         }
         if (!FILL && active) counts[qi] = mine;
+        if (DIGEST && active) fps[qi] = hash;
         if (!FILL && rp.pool) {
             const bool ok = rec_tile && nrec <= rp.cap;
             if (lane == 0) {

@@ -30,10 +30,10 @@ def pipeline(points, curve, n_max):
 
 
 def far_patch_cloud(n=120_000, seed=7):
-    """A dense 2 m patch plus two far corner points: cube side ~3000 m (cfg3's extent), so r = 0.05
+    """A dense 1 m patch plus two far corner points: cube side ~3000 m (cfg3's extent), so r = 0.05
     leaves the FP32 filter disabled (d = 2^-22 * 3000 = 7.2e-4 > 0.01 r) while mu stays ~10-20."""
     rng = np.random.default_rng(seed)
-    pts = rng.uniform(0.0, 2.0, (n, 3)) + np.array([1500.0, 1500.0, 20.0])
+    pts = rng.uniform(0.0, 1.0, (n, 3)) + np.array([1500.0, 1500.0, 20.0])
     pts[0] = (0.0, 0.0, 0.0)
     pts[1] = (3000.0, 3000.0, 60.0)
     return pts
@@ -91,7 +91,7 @@ def test_forced_fp64_kernels(ctx, ref, oracle, monkeypatch, curve):
 def test_record_overflow_fill_walk(ctx, ref, oracle, monkeypatch, cap):
     """LO_REC_CAP: tiles with more processed buffers than the cap are not recorded and are filled
     by the second walk over a tile list (radius_pt_kernel<SHAPE, true>), Lin and Struct."""
-    pts = oracle.gen_terrain(150_000, 5, 400.0)
+    pts = oracle.gen_terrain(150_000, 5, 120.0)
     p = ref.pipeline(pts, 1, 32)
     coded, tree = pipeline(pts, 1, 32)
     monkeypatch.setenv("LO_REC_CAP", str(cap))
@@ -111,6 +111,36 @@ def test_two_walk_radius_path(ctx, ref, oracle, monkeypatch):
     for r in (0.5, 2.0, 6.0):
         for shape in (0, 1):
             check_radius(tree, coded, p, r, shape=shape)
+
+
+def test_fused_digest_pass(ctx, ref, oracle, monkeypatch):
+    """LO_DIGEST_FUSED=1: row digests hashed by the count pass as members are found (in row order)
+    instead of the stand-alone radius_digest kernel over the CSR; both equal the reference."""
+    pts = oracle.gen_mixed(90_000, 13)
+    p = ref.pipeline(pts, 1, 64)
+    coded, tree = pipeline(pts, 1, 64)
+    for r in (0.7, 3.0):
+        check_radius(tree, coded, p, r)
+        monkeypatch.setenv("LO_DIGEST_FUSED", "1")
+        check_radius(tree, coded, p, r)
+        check_radius(tree, coded, p, r, shape=1)
+        monkeypatch.delenv("LO_DIGEST_FUSED")
+
+
+@pytest.mark.parametrize("legacy", ["0", "1"])
+def test_knn_kernels_k_up_to_64(ctx, ref, oracle, monkeypatch, legacy):
+    """k <= 64 runs the warp-cooperative kernel (knn_warp.cuh); LO_KNN_LEGACY=1 the per-lane-heap
+    one (still the path for k > 64).  Full mode and RandomSubset (per-query seed windows)."""
+    pts = oracle.gen_mixed(70_000, 17)
+    p = ref.pipeline(pts, 1, 64)
+    coded, tree = pipeline(pts, 1, 64)
+    monkeypatch.setenv("LO_KNN_LEGACY", legacy)
+    for k in (1, 2, 8, 16, 31, 32, 33, 48, 64):
+        check_knn(tree, coded, p, k)
+        want = p.knn(k, mode=1, subset=3000, seed=k)
+        got = lo.run_knn_batch(tree, coded, k, lo.BatchOptions(mode=lo.BatchMode.RandomSubset, subset_size=3000,
+                                                               seed=k))
+        assert np.array_equal(got.fingerprints, want["fps"]), k
 
 
 def test_knobs_off_again(ctx, ref, oracle):
