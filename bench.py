@@ -442,6 +442,7 @@ class Arm:
         e0.record(self.stream)
         for _ in range(steps):
             fn()
+        self.check(self.L.lo_context_join(self.ctx.h))  # side-stream work (aux digests, downloads) inside e1
         e1.record(self.stream)
         torch.cuda.synchronize()
         self.barrier()

@@ -104,6 +104,19 @@ int lo_context_destroy(lo_context* ctx);
 /* Waits for the context's compute and copy streams (async downloads included). */
 int lo_context_synchronize(lo_context* ctx);
 void* lo_context_stream(lo_context* ctx);
+/* Makes the context stream wait (on the device, no host sync) for the work the library put on
+ * its side streams (row digests on the aux stream, async downloads) -- e.g. before recording an
+ * end-of-region event on the context stream. */
+int lo_context_join(lo_context* ctx);
+/* Context options.
+ *   LO_OPT_CENTRE_ORDER (default 1): explicit centre lists (RandomSubset, caller order) are
+ *     searched along the curve and their rows scattered back; 0 searches them in the caller's
+ *     order (the storage-order ablation, cfg4) -- same results, slower on scattered lists.
+ *   LO_OPT_RELEASE_SCRATCH (value 1): frees the persistent radius record arena (sized for the
+ *     largest batch so far, capped at a quarter of the free memory when it grows) and the cache
+ *     of parked result buffers, for callers that share the GPU between batches. */
+enum { LO_OPT_CENTRE_ORDER = 1, LO_OPT_RELEASE_SCRATCH = 2 };
+int lo_context_set_option(lo_context* ctx, int option, int64_t value);
 /* Per-stage device timers (CUDA events on the context stream); off by default. */
 int lo_context_set_timing(lo_context* ctx, int enabled);
 /* Copies up to cap (name, ms) pairs of the last timed operations; returns count. */

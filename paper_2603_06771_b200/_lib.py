@@ -43,6 +43,8 @@ SIGNATURES = {
     "lo_context_destroy": (cint, [P]),
     "lo_context_synchronize": (cint, [P]),
     "lo_context_stream": (P, [P]),
+    "lo_context_join": (cint, [P]),
+    "lo_context_set_option": (cint, [P, cint, C.c_int64]),
     "lo_context_set_timing": (cint, [P, cint]),
     "lo_context_stage_times": (cint, [P, P, cint, P, cint]),
     "lo_device_alloc": (cint, [P, u64, PP]),

@@ -520,6 +520,7 @@ int lo_context_destroy(lo_context* ctx) {
         }
         if (ctx->pinned_scratch) cudaFreeHost(ctx->pinned_scratch);
         if (ctx->arena) cudaFree(ctx->arena);
+        if (ctx->hilbert3) cudaFree(ctx->hilbert3);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -536,6 +537,37 @@ int lo_context_synchronize(lo_context* ctx) {
     });
 }
 void* lo_context_stream(lo_context* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int lo_context_join(lo_context* ctx) {
+    return api_ctx(ctx, [&] {
+        for (cudaStream_t s : {ctx->aux_stream, ctx->copy_stream}) {
+            cudaEvent_t ev;
+            LO_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            LO_CUDA(cudaEventRecord(ev, s));
+            LO_CUDA(cudaStreamWaitEvent(ctx->stream, ev, 0));
+            cudaEventDestroy(ev);
+        }
+    });
+}
+
+int lo_context_set_option(lo_context* ctx, int option, int64_t value) {
+    return api_ctx(ctx, [&] {
+        switch (option) {
+            case LO_OPT_CENTRE_ORDER: ctx->centre_sort = value != 0; break;
+            case LO_OPT_RELEASE_SCRATCH:
+                if (value) {
+                    sync(ctx);
+                    if (ctx->arena) cudaFree(ctx->arena);
+                    ctx->arena = nullptr;
+                    ctx->arena_bytes = 0;
+                    cache_drain(ctx);
+                    sync(ctx);
+                }
+                break;
+            default: throw Error(LO_INVALID_ARGUMENT, "unknown context option");
+        }
+    });
+}
 
 int lo_context_set_timing(lo_context* ctx, int enabled) {
     return api_ctx(ctx, [&] {

@@ -405,8 +405,12 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
         const int blocks = static_cast<int>(std::max<u64>(
             1, std::min<u64>((tiles + warps - 1) / warps, static_cast<u64>(ctx->sm_count) * per_sm)));
         stage_begin(ctx, "knn");
-        // k <= 64: the warp-cooperative kernel (knn_warp.cuh); LO_KNN_LEGACY=1 keeps the per-lane heaps
-        const bool warp_kernel = use_float && kh <= 64 && !env_flag("LO_KNN_LEGACY");
+        // LO_KNN_WARP=1: the warp-cooperative kernel (knn_warp.cuh, k <= 64).  Exact, but measured 4-6x
+        // slower than the per-lane heaps (cfg1 k = 8/16/32/64: 31.9/44.6/120/386 vs 6.6/11.0/21.6/59.6 ms):
+        // every insertion is a warp-wide shuffle chain serialised per query, and the seed window offers
+        // ~k candidates to each of the 32 queries one query at a time (the per-lane heaps take them in
+        // parallel).  Kept as the measured alternative; DESIGN.md §8.
+        const bool warp_kernel = use_float && kh <= 64 && env_flag("LO_KNN_WARP");
         if (q.m && warp_kernel) {
             float E = static_cast<float>(std::ldexp(std::max(c->bmax, q.bmax), -23));
             E = std::nextafter(E, INFINITY);  // round up
@@ -530,11 +534,13 @@ int lo_knn(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, uint32
         ensure_float_shadows(ctx, coded, tree);
         u32* cidx = upload_centres(ctx, centres_host, m, coded->n);
         // explicit centres are searched in curve order, rows scattered back (centres.cu)
-        SortedCentres sc = sort_centres(ctx, cidx, centres_host ? m : 0);
-        Queries q{coded->x, coded->y, coded->z, centres_host ? sc.idx : nullptr, rows, coded->pf, coded->bmax};
+        const bool sorted = centres_host && ctx->centre_sort;  // LO_OPT_CENTRE_ORDER
+        SortedCentres sc = sort_centres(ctx, cidx, sorted ? m : 0);
+        Queries q{coded->x, coded->y, coded->z, centres_host ? (sorted ? sc.idx : cidx) : nullptr, rows, coded->pf,
+                  coded->bmax};
         try {
             *out = knn_search(ctx, tree, coded, k, q, fingerprint != 0, centres_host ? kSeedSortedIdx : 0);
-            if (centres_host) unsort_knn(ctx, sc, *out);
+            if (sorted) unsort_knn(ctx, sc, *out);
         } catch (...) {
             dfree(ctx, cidx), dfree(ctx, sc.idx), dfree(ctx, sc.pos);
             throw;

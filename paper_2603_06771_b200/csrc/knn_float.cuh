@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
             // curve; a sparse tile (random subset) seeds every lane from its own centre's window
             t0 = q.idx[tile * 32];
             t1 = static_cast<i64>(q.idx[min(q.m, tile * 32 + 32) - 1]) + 1;
-            if (t1 - t0 > 4 * 32) {
+            if (t1 - t0 > 4 * 32 || t1 <= t0) {  // spread out (or unsorted: caller's order)
                 t1 = -1;
                 if (active) {
                     const i64 c = q.idx[qi];

@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(32 * kKwWarps) knn_warp_kernel(
         } else if (seed_base == kSeedSortedIdx) {
             t0 = q.idx[tile * 32];
             t1 = static_cast<i64>(q.idx[min(q.m, tile * 32 + 32) - 1]) + 1;
-            if (t1 - t0 > 4 * 32) {
+            if (t1 - t0 > 4 * 32 || t1 <= t0) {  // spread out (or unsorted: caller's order)
                 t1 = -1;
                 // per query: its own window, offered to it alone
                 for (u32 am = act; am;) {

@@ -22,6 +22,7 @@
 namespace lo {
 
 using u8 = std::uint8_t;
+using u16 = std::uint16_t;
 using u32 = std::uint32_t;
 using u64 = std::uint64_t;
 using i32 = std::int32_t;
@@ -143,6 +144,8 @@ struct lo_context {
     // kernels whose dynamic shared-memory limit was raised on this context's device (function
     // attributes are per device; the flag lives under the context lock)
     unsigned smem_attrs = 0;
+    void* hilbert3 = nullptr;  // three-level Hilbert encode table on this device (reorder.cu)
+    bool centre_sort = true;   // LO_OPT_CENTRE_ORDER: search explicit centre lists in curve order
 };
 
 namespace lo {

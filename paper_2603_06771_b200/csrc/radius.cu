@@ -288,7 +288,7 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
             // LO_DIGEST_AUX=1: the digests trail on the aux stream, overlapping the caller's next
             // batch.  Off by default: with the count kernels issue-bound, the overlap cost more than
             // it hid (cfg1 e2e 28.6 ms with it, 28.2 ms inline).
-            static const bool aux_digest = std::getenv("LO_DIGEST_AUX") != nullptr;
+            const bool aux_digest = env_flag("LO_DIGEST_AUX");
             if (q.m && !ctx->timing && aux_digest) {
                 // the digests trail on the aux stream while the caller's next batch counts;
                 // readers of fps / indices (downloads, unsort, release) order behind `digested`
@@ -386,13 +386,17 @@ int lo_radius(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int
         ensure_float_shadows(ctx, coded, tree);
         u32* cidx = upload_centres(ctx, centres_host, m, coded->n);
         // explicit centres are searched in curve order, rows scattered back (centres.cu)
-        SortedCentres sc = sort_centres(ctx, cidx, centres_host ? m : 0);
-        Queries q{coded->x, coded->y, coded->z, centres_host ? sc.idx : nullptr, rows, coded->pf, coded->bmax};
+        // explicit centres are searched in curve order and the rows scattered back (centres.cu),
+        // unless the caller asked for its own order (lo_context_set_option LO_OPT_CENTRE_ORDER = 0)
+        const bool sorted = centres_host && ctx->centre_sort;
+        SortedCentres sc = sort_centres(ctx, cidx, sorted ? m : 0);
+        Queries q{coded->x, coded->y, coded->z, centres_host ? (sorted ? sc.idx : cidx) : nullptr, rows, coded->pf,
+                  coded->bmax};
         try {
             *out = method == LO_METHOD_STRUCT
                        ? radius_struct_search(ctx, tree, coded, shape, radius, q, fingerprint != 0)
                        : radius_search(ctx, tree, coded, shape, radius, q, fingerprint != 0);
-            if (centres_host) unsort_csr(ctx, sc, *out);
+            if (sorted) unsort_csr(ctx, sc, *out);
         } catch (...) {
             dfree(ctx, cidx), dfree(ctx, sc.idx), dfree(ctx, sc.pos);
             throw;

@@ -65,7 +65,11 @@ struct EncodeParams {
     int level;
     int curve;
     u8 enc[32 * 8];   // Hilbert / Morton encode table (state, octant) -> digit | next << 3
+    const u16* h3;    // Hilbert: three levels per step, (state, 9 Morton bits) -> 9 code bits | next << 9
 };
+
+constexpr int kH3States = 24;
+constexpr int kH3Entries = kH3States * 512;
 
 // axis_cell (sfc.hpp:120-124): floor((v - lo) * scale), clamped to [0, top].
 __device__ __forceinline__ u32 axis_cell(double v, double lo, double scale, double top) {
@@ -75,19 +79,36 @@ __device__ __forceinline__ u32 axis_cell(double v, double lo, double scale, doub
 }
 
 __device__ __forceinline__ u64 encode_cell(u32 cx, u32 cy, u32 cz, int level, int curve,
-                                           const u8* enc) {
-    if (curve == LO_MORTON) return (spread3(cx) << 2) | (spread3(cy) << 1) | spread3(cz);
+                                           const u8* enc, const u16* h3) {
+    // the Morton code's 3-bit digits are the octant digits g = x<<2 | y<<1 | z of every level
+    const u64 m = (spread3(cx) << 2) | (spread3(cy) << 1) | spread3(cz);
+    if (curve == LO_MORTON) return m;
     // Hilbert: walk the 24-state descent table from the root (equivalent to the Skilling
-    // transform of sfc.cpp:8-42; pinned by tests against the reference).
+    // transform of sfc.cpp:8-42; pinned by tests against the reference) -- level % 3 single
+    // levels, then three levels (9 Morton bits) per table step: 7 dependent lookups at level 21
+    // instead of 21.
     u64 code = 0;
     u32 s = 0;
-    for (int d = level - 1; d >= 0; --d) {
-        const u32 g = (((cx >> d) & 1u) << 2) | (((cy >> d) & 1u) << 1) | ((cz >> d) & 1u);
-        const u32 e = enc[s * 8 + g];
+    int d = level - 1;
+    for (; (d + 1) % 3 != 0; --d) {
+        const u32 e = enc[s * 8 + ((m >> (3 * d)) & 7u)];
         code = (code << 3) | (e & 7u);
         s = e >> 3;
     }
+    for (d -= 2; d >= 0; d -= 3) {
+        const u32 e = h3[s * 512 + ((m >> (3 * d)) & 511u)];
+        code = (code << 9) | (e & 511u);
+        s = e >> 9;
+    }
     return code;
+}
+
+// Shared-memory copy of the three-level Hilbert table (Morton never reads it).
+__device__ __forceinline__ void load_h3(u16* dst, const EncodeParams& p) {
+    if (p.curve != LO_HILBERT) return;
+    const uint4* src = reinterpret_cast<const uint4*>(p.h3);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int i = threadIdx.x; i < kH3Entries * 2 / 16; i += blockDim.x) d4[i] = src[i];
 }
 
 template <bool HIST>
@@ -95,8 +116,10 @@ __global__ void __launch_bounds__(256) encode_kernel(const double* __restrict__ 
                                                      EncodeParams p, u64* __restrict__ codes,
                                                      u32* __restrict__ hist, u32* __restrict__ err) {
     __shared__ u8 enc[32 * 8];
+    __shared__ __align__(16) u16 h3[kH3Entries];
     __shared__ u32 h[HIST ? 8 * 256 : 1];
     for (int i = threadIdx.x; i < 32 * 8; i += blockDim.x) enc[i] = p.enc[i];
+    load_h3(h3, p);
     if (HIST)
         for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) h[i] = 0;
     __syncthreads();
@@ -110,7 +133,7 @@ __global__ void __launch_bounds__(256) encode_kernel(const double* __restrict__ 
         const u32 cx = axis_cell(x, p.lo[0], p.scale[0], p.top);
         const u32 cy = axis_cell(y, p.lo[1], p.scale[1], p.top);
         const u32 cz = axis_cell(z, p.lo[2], p.scale[2], p.top);
-        const u64 code = encode_cell(cx, cy, cz, p.level, p.curve, enc);
+        const u64 code = encode_cell(cx, cy, cz, p.level, p.curve, enc, h3);
         codes[i] = code;
         if (HIST) {
 #pragma unroll
@@ -311,11 +334,13 @@ __global__ void invert_perm_kernel(const u32* __restrict__ perm, u64 n, u32* __r
 __global__ void encode_cells_kernel(const u32* __restrict__ cells, u64 n, int level, int curve,
                                     EncodeParams p, u64* __restrict__ codes) {
     __shared__ u8 enc[32 * 8];
+    __shared__ __align__(16) u16 h3[kH3Entries];
     for (int i = threadIdx.x; i < 32 * 8; i += blockDim.x) enc[i] = p.enc[i];
+    load_h3(h3, p);
     __syncthreads();
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
          i += (u64)gridDim.x * blockDim.x)
-        codes[i] = encode_cell(cells[3 * i], cells[3 * i + 1], cells[3 * i + 2], level, curve, enc);
+        codes[i] = encode_cell(cells[3 * i], cells[3 * i + 1], cells[3 * i + 2], level, curve, enc, h3);
 }
 
 __global__ void decode_codes_kernel(const u64* __restrict__ codes, u64 n, int level,
@@ -381,9 +406,34 @@ static Disc compute_disc(lo_context* ctx, const double* xyz_dev, u64 n, int leve
     return d;
 }
 
-static EncodeParams make_params(const double box[6], const double scale[3], int level,
+// The three-level Hilbert table on this context's device (built from the CurveStepper closure,
+// uploaded once per context).
+static const u16* hilbert3_table(lo_context* ctx) {
+    if (ctx->hilbert3) return static_cast<const u16*>(ctx->hilbert3);
+    const CurveTables& t = curve_tables(LO_HILBERT);
+    require(t.states == kH3States, LO_LOGIC_ERROR, "Hilbert table: unexpected state count");
+    std::vector<u16> h(kH3Entries);
+    for (int s0 = 0; s0 < kH3States; ++s0)
+        for (u32 idx = 0; idx < 512; ++idx) {
+            u32 st = static_cast<u32>(s0), code = 0;
+            for (int l = 2; l >= 0; --l) {
+                const u32 e = t.enc[st * 8 + ((idx >> (3 * l)) & 7u)];
+                code = (code << 3) | (e & 7u);
+                st = e >> 3;
+            }
+            h[s0 * 512 + idx] = static_cast<u16>(code | (st << 9));
+        }
+    void* d = nullptr;
+    LO_CUDA(cudaMalloc(&d, h.size() * sizeof(u16)));
+    LO_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(u16), cudaMemcpyHostToDevice));
+    ctx->hilbert3 = d;
+    return static_cast<const u16*>(d);
+}
+
+static EncodeParams make_params(lo_context* ctx, const double box[6], const double scale[3], int level,
                                 int curve) {
     EncodeParams p{};
+    p.h3 = curve == LO_HILBERT ? hilbert3_table(ctx) : nullptr;
     for (int a = 0; a < 3; ++a) {
         p.lo[a] = box[a];
         p.hi[a] = box[3 + a];
@@ -485,15 +535,17 @@ __global__ void __launch_bounds__(256) query_codes(const double* __restrict__ x,
                                                    const double* __restrict__ z, u64 n, EncodeParams p,
                                                    u64* __restrict__ codes, u32* __restrict__ hist) {
     __shared__ u8 enc[32 * 8];
+    __shared__ __align__(16) u16 h3[kH3Entries];
     __shared__ u32 h[8 * 256];
     for (int i = threadIdx.x; i < 32 * 8; i += blockDim.x) enc[i] = p.enc[i];
+    load_h3(h3, p);
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) h[i] = 0;
     __syncthreads();
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         const u32 cx = axis_cell(x[i], p.lo[0], p.scale[0], p.top);
         const u32 cy = axis_cell(y[i], p.lo[1], p.scale[1], p.top);
         const u32 cz = axis_cell(z[i], p.lo[2], p.scale[2], p.top);
-        const u64 code = encode_cell(cx, cy, cz, p.level, p.curve, enc);
+        const u64 code = encode_cell(cx, cy, cz, p.level, p.curve, enc, h3);
         codes[i] = code;
 #pragma unroll
         for (int b = 0; b < 8; ++b) atomicAdd(&h[b * 256 + ((code >> (8 * b)) & 0xff)], 1u);
@@ -515,7 +567,7 @@ u32* sort_points_sfc(lo_context* ctx, const lo_coded* c, const double* x, const 
         hist = dalloc_t<u32>(ctx, 8 * 256);
         pos = dalloc_t<u32>(ctx, m);
         LO_CUDA(cudaMemsetAsync(hist, 0, 8 * 256 * 4, ctx->stream));
-        const EncodeParams p = make_params(c->disc_box, c->scale, c->level, c->curve);
+        const EncodeParams p = make_params(ctx, c->disc_box, c->scale, c->level, c->curve);
         query_codes<<<std::min(grid_for(ctx, m, 256), ctx->sm_count * 4), 256, 0, ctx->stream>>>(x, y, z, m, p,
                                                                                               codes, hist);
         LO_CHECK_LAUNCH();
@@ -554,7 +606,7 @@ lo_coded* reorder_device(lo_context* ctx, const double* xyz, u64 n, int curve, i
         u64* codes = dalloc_t<u64>(ctx, n);
         u32* hist = dalloc_t<u32>(ctx, 8 * 256 + 1);
         LO_CUDA(cudaMemsetAsync(hist, 0, (8 * 256 + 1) * 4, ctx->stream));
-        const EncodeParams p = make_params(disc.box, disc.scale, level, curve);
+        const EncodeParams p = make_params(ctx, disc.box, disc.scale, level, curve);
         encode_kernel<true><<<grid_for(ctx, n, 256, 4), 256, 0, ctx->stream>>>(
             xyz, n, p, codes, hist, hist + 8 * 256);
         LO_CHECK_LAUNCH();
@@ -625,7 +677,7 @@ int lo_compute_codes(lo_context* ctx, const double* xyz_host, uint64_t n, int cu
             std::memcpy(box, d.box, sizeof box);
             std::memcpy(scale, d.scale, sizeof scale);
         }
-        const EncodeParams p = make_params(box, scale, level, curve);
+        const EncodeParams p = make_params(ctx, box, scale, level, curve);
         encode_kernel<false><<<grid_for(ctx, n, 256, 4), 256, 0, ctx->stream>>>(xyz, n, p, codes,
                                                                                 nullptr, err);
         LO_CHECK_LAUNCH();
@@ -648,7 +700,7 @@ int lo_encode_cells(lo_context* ctx, const uint32_t* cells_host, uint64_t n, int
         u64* codes = dalloc_t<u64>(ctx, n);
         LO_CUDA(cudaMemcpyAsync(cells, cells_host, 12 * n, cudaMemcpyHostToDevice, ctx->stream));
         const double box[6] = {0, 0, 0, 1, 1, 1}, scale[3] = {0, 0, 0};
-        const EncodeParams p = make_params(box, scale, level, curve);
+        const EncodeParams p = make_params(ctx, box, scale, level, curve);
         encode_cells_kernel<<<grid_for(ctx, n, 256), 256, 0, ctx->stream>>>(cells, n, level, curve,
                                                                             p, codes);
         LO_CHECK_LAUNCH();

@@ -127,14 +127,14 @@ def test_fused_digest_pass(ctx, ref, oracle, monkeypatch):
         monkeypatch.delenv("LO_DIGEST_FUSED")
 
 
-@pytest.mark.parametrize("legacy", ["0", "1"])
-def test_knn_kernels_k_up_to_64(ctx, ref, oracle, monkeypatch, legacy):
-    """k <= 64 runs the warp-cooperative kernel (knn_warp.cuh); LO_KNN_LEGACY=1 the per-lane-heap
-    one (still the path for k > 64).  Full mode and RandomSubset (per-query seed windows)."""
+@pytest.mark.parametrize("warp", ["0", "1"])
+def test_knn_kernels_k_up_to_64(ctx, ref, oracle, monkeypatch, warp):
+    """The per-lane-heap kNN kernel (default) and, with LO_KNN_WARP=1, the warp-cooperative one
+    (knn_warp.cuh, k <= 64).  Full mode and RandomSubset (per-query seed windows)."""
     pts = oracle.gen_mixed(70_000, 17)
     p = ref.pipeline(pts, 1, 64)
     coded, tree = pipeline(pts, 1, 64)
-    monkeypatch.setenv("LO_KNN_LEGACY", legacy)
+    monkeypatch.setenv("LO_KNN_WARP", warp)
     for k in (1, 2, 8, 16, 31, 32, 33, 48, 64):
         check_knn(tree, coded, p, k)
         want = p.knn(k, mode=1, subset=3000, seed=k)
