@@ -181,20 +181,18 @@ __global__ void single_leaf_tnode(TNode* tn, u32 n, u32* parent) {
 
 // Leaf boxes from their points, then bottom-up unions: the last child to arrive at a parent
 // (arrival counter) computes the parent's box and continues upward.
-// Tight boxes bottom-up.  A group of 8 lanes takes one leaf: coalesced loads of its points
-// (leaves hold ~13 points at cfg3, so a thread per leaf left 4.5 of 32 lanes busy and read 32
-// scattered lines per load), a 3-step shuffle reduction, and the group leader propagates the box
-// to the parents whose children have all arrived (arrival counters).
-__global__ void __launch_bounds__(128) tnode_boxes(TNode* tn, u64 tnodes, const double* __restrict__ x,
-                                                   const double* __restrict__ y, const double* __restrict__ z,
-                                                   const u32* __restrict__ parent, const u32* __restrict__ tid_of,
-                                                   u32* __restrict__ arrivals) {
+// Tight boxes bottom-up, in two launches.  tnode_leaf_boxes: a group of 8 lanes takes one leaf --
+// coalesced loads of its points and a 3-step shuffle reduction (leaves hold ~13 points at cfg3; a
+// thread per leaf left 4.5 of 32 lanes busy and read 32 scattered lines per load).
+// tnode_boxes: a thread per leaf carries its box to the parents whose children have all arrived
+// (arrival counters); a group leader doing that chain held its 7 lanes idle (12 ms vs 2.8 ms).
+__global__ void __launch_bounds__(128) tnode_leaf_boxes(TNode* tn, u64 tnodes, const double* __restrict__ x,
+                                                        const double* __restrict__ y,
+                                                        const double* __restrict__ z) {
     const int sub = threadIdx.x & 7;
     const u64 groups = (static_cast<u64>(gridDim.x) * blockDim.x) >> 3;
     for (u64 t = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 3; t < tnodes; t += groups) {
-        // the group stays converged: every lane of the group has the same t
-        const u32 nch = tn[t].nchild;
-        if (nch != 0) continue;
+        if (tn[t].nchild != 0) continue;  // group-uniform
         const u32 b = tn[t].begin, e = tn[t].end;
         double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
         for (u32 i = b + sub; i < e; i += 8) {
@@ -214,12 +212,17 @@ __global__ void __launch_bounds__(128) tnode_boxes(TNode* tn, u64 tnodes, const 
                 hi[a] = fmax(hi[a], __shfl_xor_sync(gm, hi[a], o));
             }
         }
-        if (sub != 0) continue;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            tn[t].lo[a] = lo[a];
-            tn[t].hi[a] = hi[a];
+        if (sub < 3) {
+            tn[t].lo[sub] = lo[sub];
+            tn[t].hi[sub] = hi[sub];
         }
+    }
+}
+
+__global__ void __launch_bounds__(128) tnode_boxes(TNode* tn, u64 tnodes, const u32* __restrict__ parent,
+                                                   const u32* __restrict__ tid_of, u32* __restrict__ arrivals) {
+    for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < tnodes; t += (u64)gridDim.x * blockDim.x) {
+        if (tn[t].nchild != 0) continue;
         u32 cur = parent[t];
         while (cur != ~0u) {
             __threadfence();
@@ -552,8 +555,9 @@ static lo_octree* finish_octree(lo_context* ctx, const lo_coded* coded, LeafBuil
         single_leaf_tnode<<<1, 1, 0, ctx->stream>>>(t->tn, static_cast<u32>(n), parent);
     }
     LO_CHECK_LAUNCH();
-    tnode_boxes<<<grid1(ctx, 8 * T, 128), 128, 0, ctx->stream>>>(t->tn, T, coded->x, coded->y,
-                                                                  coded->z, parent, tid_of, arrivals);
+    tnode_leaf_boxes<<<grid1(ctx, 8 * T, 128), 128, 0, ctx->stream>>>(t->tn, T, coded->x, coded->y, coded->z);
+    LO_CHECK_LAUNCH();
+    tnode_boxes<<<grid1(ctx, T, 128), 128, 0, ctx->stream>>>(t->tn, T, parent, tid_of, arrivals);
     LO_CHECK_LAUNCH();
     build_float_nodes(ctx, t, coded);
     dfree(ctx, tbase);

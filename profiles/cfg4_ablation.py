@@ -32,8 +32,16 @@ import bench  # noqa: E402
 from paper_2603_06771_b200 import _lib, linoct as lo  # noqa: E402
 
 
+KNN_STORAGE_CENTRES = 2_000_000  # kNN in true storage order is bounded to a prefix of the queries
+
+
 def run_order(L, ctx, xyz, n, order, stats=True):
+    """order: "morton" / "hilbert" (Full mode, sorted queries); "original" (queries in storage
+    order, searched along the curve by the library and scattered back -- the default mitigation);
+    "original_storage" (the same queries searched in storage order: LO_OPT_CENTRE_ORDER = 0)."""
     curve = 0 if order == "morton" else 1
+    storage = order == "original_storage"
+    _lib.check(L.lo_context_set_option(ctx.h, 1, 0 if storage else 1))
     ctx.set_timing(True)
     coded = C.c_void_p()
     _lib.check(L.lo_reorder(ctx.h, xyz.ctypes.data, n, curve, 21, C.byref(coded)))
@@ -47,7 +55,7 @@ def run_order(L, ctx, xyz, n, order, stats=True):
             rec[f"{k}_ms"] = st[k]
             rec[f"{k}_keys_per_s"] = n / (st[k] * 1e-3)
     centres = None
-    if order == "original":
+    if order.startswith("original"):
         perm = np.empty(n, np.uint32)
         _lib.check(L.lo_coded_download(ctx.h, coded, None, None, perm.ctypes.data))
         inv = np.empty(n, np.uint32)
@@ -67,18 +75,22 @@ def run_order(L, ctx, xyz, n, order, stats=True):
     rec["radius_r3_ms"] = info.device_ms
     rec["radius_r3_wall_ms"] = wall * 1e3
     rec["radius_mu"] = info.mean_count
+    km = m
+    if order.startswith("original"):
+        km = min(m, KNN_STORAGE_CENTRES)  # the same bounded prefix for both original-order rows
+        rec["knn16_centres"] = km
     for rep in range(2):
         kh = C.c_void_p()
-        _lib.check(L.lo_knn(ctx.h, tree, coded, 16, cp, m, 1, C.byref(kh)))
+        _lib.check(L.lo_knn(ctx.h, tree, coded, 16, cp, km, 1, C.byref(kh)))
         rows, keff, ms = C.c_uint64(), C.c_uint32(), C.c_double()
         _lib.check(L.lo_knn_info_get(kh, C.byref(rows), C.byref(keff), C.byref(ms)))
         L.lo_knn_destroy(kh)
     rec["knn16_ms"] = ms.value
-    if stats:
+    if stats and not storage:  # (the storage-order row shares the "original" histogram)
         # exact locality histogram over every centre (sorted-order kNN result), mapped through
         # the permutation for the original order
         perm = None
-        if order == "original":
+        if order.startswith("original"):
             perm = np.empty(n, np.uint32)
             _lib.check(L.lo_coded_download(ctx.h, coded, None, None, perm.ctypes.data))
         full = C.c_void_p()
@@ -101,6 +113,7 @@ def run_order(L, ctx, xyz, n, order, stats=True):
                            "log2_bins": [int(x) for x in log2]}
     L.lo_octree_destroy(tree)
     L.lo_coded_destroy(coded)
+    _lib.check(L.lo_context_set_option(ctx.h, 1, 1))
     return rec
 
 
@@ -108,7 +121,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=50_000_000)
     ap.add_argument("--out", default=None)
-    ap.add_argument("--order", nargs="*", default=["original", "morton", "hilbert"])
+    ap.add_argument("--order", nargs="*", default=["original_storage", "original", "morton", "hilbert"])
     ap.add_argument("--searches-only", action="store_true")
     a = ap.parse_args()
     cfg = dict(bench.CONFIGS["cfg4"])
