@@ -9,7 +9,8 @@ reordered coordinates, LeafArray, InternalNode table); radius counts and FNV-1a 
 compared on `--centres` seeded random centres (RandomSubset, the reference's own sampler) and
 kNN digests on a quarter of that.  cfg0 is compared on ALL centres.  At 100M points the
 reference cannot hold every CSR row in memory, which is exactly why it digests them
-(search.cpp:263-271).  Also runnable through pytest: LO_SCALE=1 pytest tests/test_scale.py.
+(search.cpp:263-271).  The same comparisons run in the driver's GPU suite as
+tests/test_gpu_scale.py (cfg1 / cfg4 / cfg3 in Full mode and a 250k-centre cfg3 RandomSubset).
 """
 from __future__ import annotations
 
