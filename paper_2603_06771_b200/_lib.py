@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblinoct_b200.so")
+# LO_LIB_PATH: a side build of a tuning variant (build.py with LO_BUILD_DIR); the product path is the in-tree .so
+LIB_PATH = os.environ.get("LO_LIB_PATH") or os.path.join(HERE, "liblinoct_b200.so")
 HEADER = os.path.join(HERE, "..", "include", "linoct_b200.h")
 
 P = C.c_void_p

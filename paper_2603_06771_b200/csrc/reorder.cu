@@ -156,7 +156,15 @@ __global__ void __launch_bounds__(256) encode_kernel(const double* __restrict__ 
 // (key, value) exactly once.
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 16;
+// 12 keys per thread, 4 blocks per SM (48 KB of shared memory each): cfg3 sort 9.50 -> 8.85 ms,
+// cfg1 1.145 -> 1.023 ms against 16 / 3 (8 / 5: 10.18 / 1.089; 16 / 4: 9.35 / 1.111; sort_probe.py)
+#ifndef LO_SORT_ITEMS
+#define LO_SORT_ITEMS 12
+#endif
+#ifndef LO_SORT_MINB
+#define LO_SORT_MINB 4
+#endif
+constexpr int kSortItems = LO_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr u64 kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kFlagMask = 3ull << 62;
 
@@ -171,7 +179,7 @@ struct SortSmem {
 };
 
 template <bool FIRST>
-__global__ void __launch_bounds__(kSortThreads, 3) onesweep_pass(
+__global__ void __launch_bounds__(kSortThreads, LO_SORT_MINB) onesweep_pass(
     const u64* __restrict__ kin, const u32* __restrict__ vin, u64* __restrict__ kout,
     u32* __restrict__ vout, u64 n, int shift, const u64* __restrict__ digit_base,
     u64* status, u32* counter) {
