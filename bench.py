@@ -96,7 +96,8 @@ def generate_oracle(cfg):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 25 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (every LO_BENCH_CLOCK_MS,
+    default 100 ms; 0 disables it)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -108,10 +109,13 @@ class ClockSampler:
         self.lines: list[str] = []
 
     def __enter__(self):
+        interval = int(os.environ.get("LO_BENCH_CLOCK_MS", "100"))
+        if interval <= 0:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "25"],
+                 "--format=csv,noheader,nounits", "-lms", str(interval)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -440,21 +444,36 @@ class Arm:
         self.barrier()
         torch.cuda.synchronize()
         e0.record(self.stream)
+        per = [] if os.environ.get("LO_BENCH_STEP_TIMES") else None  # diagnostics: per-call device times
         for _ in range(steps):
             fn()
+            if per is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(self.stream)
+                per.append(ev)
         self.check(self.L.lo_context_join(self.ctx.h))  # side-stream work (aux digests, downloads) inside e1
         e1.record(self.stream)
         torch.cuda.synchronize()
         self.barrier()
+        if per:
+            prev, out = e0, []
+            for ev in per:
+                out.append(round(prev.elapsed_time(ev), 2))
+                prev = ev
+            sys.stderr.write(f"[bench] per-call device ms: {out}\n")
         return self.max_over_ranks(e0.elapsed_time(e1) / steps)
 
     def main_region(self, steps, warmup):
         for _ in range(warmup):
             self.step()
         self.ctx.synchronize()
+        if os.environ.get("LO_DEBUG_ALLOC"):
+            sys.stderr.write("== timed region\n")
         l0 = self.L.lo_launch_count()
         with ClockSampler(self.local) as clocks:
             ms = self.timed(self.step, steps)
+        if os.environ.get("LO_DEBUG_ALLOC"):
+            sys.stderr.write("== end of timed region\n")
         return ms, self.L.lo_launch_count() - l0, clocks.summary()
 
     def stages(self, reps):

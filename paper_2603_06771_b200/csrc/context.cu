@@ -3,6 +3,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdio>
 #include <mutex>
@@ -29,6 +30,7 @@ void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
 }
 
 void reclaim(lo_context* ctx, bool wait) {
+    SlowLog slow("reclaim", ctx->deferred.size());
     auto& d = ctx->deferred;
     for (size_t i = 0; i < d.size();) {
         if (wait) cudaEventSynchronize(d[i].done);
@@ -44,8 +46,30 @@ void reclaim(lo_context* ctx, bool wait) {
     }
 }
 
-constexpr size_t kBigBytes = 64ull << 20;  // buffers from this size go through the cache
-constexpr size_t kCacheEntries = 16;
+// Large device buffers (>= 64 MB) are recycled by the context instead of the stream-ordered pool.
+// A step of the hot path allocates and frees the same ~25 large buffers every time (the coded cloud's
+// SoA arrays, the sort's ping-pong arrays, the tree's tables, the 25 GB CSR...), and whenever the pool
+// has no free block of the right shape it maps new physical memory inside cudaMallocAsync: 2-4 ms
+// per 400-800 MB and 140 ms for the 25 GB CSR, with the GPU idle meanwhile -- cfg3 steps varied
+// between 85 and 117 ms on identical kernels.  dalloc() hands out a parked buffer of the right size
+// when there is one; dfree() / big_release() park it again (behind an event when its last reader is
+// another stream).  Parked buffers go back to the pool when the cache is over its limit, on
+// lo_context_synchronize, or when an allocation fails.
+constexpr size_t kBigBytes = 64ull << 20;
+constexpr size_t kCacheEntries = 48;
+// parked bytes are capped too (oldest finished first): what the cache holds the pool cannot reuse
+// for other shapes, and a pool that has to grow is what made the allocations slow
+static size_t cache_byte_cap(lo_context* ctx) {
+    if (!ctx->cache_cap) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+            cudaGetLastError();
+            total_b = 64ull << 30;
+        }
+        ctx->cache_cap = total_b / 2;
+    }
+    return ctx->cache_cap;
+}
 
 static bool cache_ready(const lo_context::Cached& c) {
     if (!c.ready) return true;  // last used on ctx->stream: stream order makes it reusable
@@ -62,40 +86,70 @@ static void cache_free(lo_context* ctx, lo_context::Cached& c) {
     cudaFreeAsync(c.p, ctx->stream);
 }
 
-void* big_alloc(lo_context* ctx, size_t bytes, size_t* got) {
-    *got = bytes;
-    if (bytes >= kBigBytes) {
-        auto& c = ctx->cache;
-        int best = -1;
-        for (size_t i = 0; i < c.size(); ++i) {
-            if (c[i].bytes < bytes || c[i].bytes > bytes + bytes / 2 + kBigBytes) continue;
-            if (!cache_ready(c[i])) continue;
-            if (best < 0 || c[i].bytes < c[best].bytes) best = static_cast<int>(i);
-        }
-        if (best >= 0) {
-            void* p = c[best].p;
-            *got = c[best].bytes;
-            if (c[best].ready) cudaEventDestroy(c[best].ready);
-            c.erase(c.begin() + best);
-            return p;
-        }
-    }
-    return dalloc(ctx, bytes);
+void cache_drain(lo_context* ctx) {
+    for (auto& c : ctx->cache) cache_free(ctx, c);
+    ctx->cache.clear();
 }
 
-void big_release(lo_context* ctx, void* p, size_t bytes, cudaStream_t last_use) {
-    if (!p) return;
-    if (bytes < kBigBytes) {
-        if (last_use == ctx->stream) {
-            dfree(ctx, p);
-        } else {  // release once the other stream's reader has finished
-            lo_context::Deferred d{nullptr, {p}};
-            LO_CUDA(cudaEventCreateWithFlags(&d.done, cudaEventDisableTiming));
-            LO_CUDA(cudaEventRecord(d.done, last_use));
-            ctx->deferred.push_back(std::move(d));
-        }
-        return;
+static void* pool_alloc(lo_context* ctx, size_t bytes) {
+    void* p = nullptr;
+    static const bool dbg_alloc = std::getenv("LO_DEBUG_ALLOC") != nullptr;
+    const auto t0 = dbg_alloc ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
+    cudaError_t e = cudaMallocAsync(&p, bytes, ctx->stream);
+    if (e != cudaSuccess && !ctx->cache.empty()) {  // parked buffers go back first
+        cudaGetLastError();
+        if (dbg_alloc) std::fprintf(stderr, "[lo] alloc %zu B failed: draining %zu parked buffers\n", bytes, ctx->cache.size());
+        cache_drain(ctx);
+        e = cudaMallocAsync(&p, bytes, ctx->stream);
     }
+    if (dbg_alloc) {
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms > 0.2) std::fprintf(stderr, "[lo] cudaMallocAsync %zu B took %.2f ms\n", bytes, ms);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        char buf[160];
+        std::snprintf(buf, sizeof buf, "device allocation of %zu bytes failed (%s)", bytes, cudaGetErrorName(e));
+        throw Error(LO_OUT_OF_MEMORY, buf);
+    }
+    return p;
+}
+
+void* dalloc(lo_context* ctx, size_t bytes) {
+    SlowLog slow("dalloc", bytes);
+    if (!ctx->deferred.empty()) reclaim(ctx, false);
+    if (bytes < kBigBytes) return pool_alloc(ctx, bytes);
+    auto& c = ctx->cache;
+    int best = -1;
+    for (size_t i = 0; i < c.size(); ++i) {
+        if (c[i].bytes < bytes || c[i].bytes > bytes + bytes / 2 + kBigBytes) continue;
+        if (!cache_ready(c[i])) continue;
+        if (best < 0 || c[i].bytes < c[best].bytes) best = static_cast<int>(i);
+    }
+    void* p;
+    size_t got = bytes;
+    if (best >= 0) {
+        p = c[best].p;
+        got = c[best].bytes;
+        if (c[best].ready) cudaEventDestroy(c[best].ready);
+        c.erase(c.begin() + best);
+    } else {
+        p = pool_alloc(ctx, bytes);
+    }
+    ctx->big[p] = got;
+    return p;
+}
+
+void* big_alloc(lo_context* ctx, size_t bytes, size_t* got) {
+    void* p = dalloc(ctx, bytes);
+    const auto it = ctx->big.find(p);
+    *got = it != ctx->big.end() ? it->second : 0;  // 0: a small buffer (plain pool)
+    return p;
+}
+
+// Parks a large buffer (its last reader: `last_use`), trimming the cache to its limit.
+static void park(lo_context* ctx, void* p, size_t bytes, cudaStream_t last_use) {
+    SlowLog slow("park", bytes);
     lo_context::Cached c{p, bytes, nullptr};
     if (last_use != ctx->stream) {
         LO_CUDA(cudaEventCreateWithFlags(&c.ready, cudaEventDisableTiming));
@@ -103,9 +157,13 @@ void big_release(lo_context* ctx, void* p, size_t bytes, cudaStream_t last_use) 
     }
     auto& cache = ctx->cache;
     cache.push_back(c);
-    // over the limit the oldest finished buffers go back to the pool (waiting only if none has)
-    for (size_t i = 0; i < cache.size() && cache.size() > kCacheEntries;) {
+    size_t parked = 0;
+    for (const auto& e : cache) parked += e.bytes;
+    const size_t cap = cache_byte_cap(ctx);
+    // over the limits the oldest finished buffers go back to the pool (waiting only if none has)
+    for (size_t i = 0; i < cache.size() && (cache.size() > kCacheEntries || parked > cap);) {
         if (cache_ready(cache[i])) {
+            parked -= cache[i].bytes;
             cache_free(ctx, cache[i]);
             cache.erase(cache.begin() + i);
         } else {
@@ -118,35 +176,54 @@ void big_release(lo_context* ctx, void* p, size_t bytes, cudaStream_t last_use) 
     }
 }
 
-void cache_drain(lo_context* ctx) {
-    for (auto& c : ctx->cache) cache_free(ctx, c);
-    ctx->cache.clear();
-}
-
-void* dalloc(lo_context* ctx, size_t bytes) {
-    if (!ctx->deferred.empty()) reclaim(ctx, false);
-    void* p = nullptr;
-    cudaError_t e = cudaMallocAsync(&p, bytes, ctx->stream);
-    if (e != cudaSuccess && !ctx->cache.empty()) {  // parked buffers go back first
-        cudaGetLastError();
-        cache_drain(ctx);
-        e = cudaMallocAsync(&p, bytes, ctx->stream);
+void big_release(lo_context* ctx, void* p, size_t /*bytes*/, cudaStream_t last_use) {
+    if (!p) return;
+    const auto it = ctx->big.find(p);
+    if (it != ctx->big.end()) {
+        const size_t size = it->second;
+        ctx->big.erase(it);
+        park(ctx, p, size, last_use);
+        return;
     }
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        char buf[160];
-        std::snprintf(buf, sizeof buf, "device allocation of %zu bytes failed (%s)", bytes,
-                      cudaGetErrorName(e));
-        throw Error(LO_OUT_OF_MEMORY, buf);
+    if (last_use == ctx->stream) {
+        cudaFreeAsync(p, ctx->stream);
+    } else {  // release once the other stream's reader has finished
+        lo_context::Deferred d{nullptr, {p}};
+        LO_CUDA(cudaEventCreateWithFlags(&d.done, cudaEventDisableTiming));
+        LO_CUDA(cudaEventRecord(d.done, last_use));
+        ctx->deferred.push_back(std::move(d));
     }
-    return p;
 }
 
 void dfree(lo_context* ctx, void* p) {
-    if (p) cudaFreeAsync(p, ctx->stream);
+    if (!p) return;
+    const auto it = ctx->big.find(p);
+    if (it != ctx->big.end()) {
+        const size_t size = it->second;
+        ctx->big.erase(it);
+        park(ctx, p, size, ctx->stream);
+        return;
+    }
+    cudaFreeAsync(p, ctx->stream);
 }
 
-void sync(lo_context* ctx) { LO_CUDA(cudaStreamSynchronize(ctx->stream)); }
+// Host waits inside a batch (a histogram or total the host needs next) spin on an event query
+// instead of cudaStreamSynchronize: a blocking wait may sleep the thread, and its wake-up latency
+// left the GPU idle at each of the ~8 such points of a step -- identical kernels, cfg3 steps of 85
+// or 91-93 ms depending on the run.
+void spin_wait(cudaEvent_t ev) {
+    for (;;) {
+        const cudaError_t e = cudaEventQuery(ev);
+        if (e == cudaSuccess) return;
+        if (e != cudaErrorNotReady) LO_CUDA(e);
+    }
+}
+
+void sync(lo_context* ctx) {
+    if (!ctx->sync_ev) LO_CUDA(cudaEventCreateWithFlags(&ctx->sync_ev, cudaEventDisableTiming));
+    LO_CUDA(cudaEventRecord(ctx->sync_ev, ctx->stream));
+    spin_wait(ctx->sync_ev);
+}
 
 __global__ void fetch_words(const u32* __restrict__ src, u32* dst, u32 words) {
     for (u32 i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
@@ -161,6 +238,7 @@ void fetch_small(lo_context* ctx, const void* dev, size_t bytes) {
 }
 
 void* arena(lo_context* ctx, size_t bytes) {
+    SlowLog slow("arena", bytes);
     if (ctx->arena_bytes >= bytes) return ctx->arena;
     if (ctx->arena) {
         sync(ctx);
@@ -519,6 +597,7 @@ int lo_context_destroy(lo_context* ctx) {
             cudaEventDestroy(s.b);
         }
         if (ctx->pinned_scratch) cudaFreeHost(ctx->pinned_scratch);
+        if (ctx->sync_ev) cudaEventDestroy(ctx->sync_ev);
         if (ctx->arena) cudaFree(ctx->arena);
         if (ctx->hilbert3) cudaFree(ctx->hilbert3);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -532,8 +611,7 @@ int lo_context_synchronize(lo_context* ctx) {
         LO_CUDA(cudaStreamSynchronize(ctx->copy_stream));
         LO_CUDA(cudaStreamSynchronize(ctx->h2d_stream));
         LO_CUDA(cudaStreamSynchronize(ctx->aux_stream));
-        reclaim(ctx, true);
-        cache_drain(ctx);  // parked result buffers go back to the pool (bounded between syncs)
+        reclaim(ctx, true);  // parked large buffers stay parked (bounded; LO_OPT_RELEASE_SCRATCH frees them)
     });
 }
 void* lo_context_stream(lo_context* ctx) { return ctx ? ctx->stream : nullptr; }
@@ -560,6 +638,7 @@ int lo_context_set_option(lo_context* ctx, int option, int64_t value) {
                     if (ctx->arena) cudaFree(ctx->arena);
                     ctx->arena = nullptr;
                     ctx->arena_bytes = 0;
+                    ctx->arena_budgeted = 0;
                     cache_drain(ctx);
                     sync(ctx);
                 }
@@ -634,7 +713,7 @@ int lo_d2h_fence(lo_context* ctx, int slot) {
 int lo_d2h_wait(lo_context* ctx, int slot) {
     return api_ctx(ctx, [&] {
         require(slot >= 0 && slot < lo_context::kH2dSlots, LO_INVALID_ARGUMENT, "d2h slot out of range");
-        LO_CUDA(cudaEventSynchronize(ctx->d2h_done[slot]));
+        spin_wait(ctx->d2h_done[slot]);
         reclaim(ctx, false);
     });
 }

@@ -111,6 +111,7 @@ constexpr int kKnnSmemBudget = 200 * 1024;
 
 #include "knn_float.cuh"
 #include "knn_warp.cuh"
+#include "knn_select.cuh"
 
 namespace lo {
 
@@ -399,11 +400,57 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
             }
         }
         const size_t smem = warps * (per_warp_fixed + (global_heap ? 0 : per_warp_heap));
-        const u64 tiles = (q.m + 31) / 32;
         int per_sm = std::max(1, static_cast<int>(220 * 1024 / std::max<size_t>(smem, 1)));
         per_sm = std::min(per_sm, 16);
-        const int blocks = static_cast<int>(std::max<u64>(
-            1, std::min<u64>((tiles + warps - 1) / warps, static_cast<u64>(ctx->sm_count) * per_sm)));
+        auto grid_for = [&](u64 rows) {
+            const u64 tl = (rows + 31) / 32;
+            return static_cast<int>(std::max<u64>(
+                1, std::min<u64>((tl + warps - 1) / warps, static_cast<u64>(ctx->sm_count) * per_sm)));
+        };
+        const u64 tiles = (q.m + 31) / 32;
+        const int blocks = grid_for(q.m);
+        float E = static_cast<float>(std::ldexp(std::max(c->bmax, q.bmax), -23));
+        E = std::nextafter(E, INFINITY);  // round up
+        // the FP32-filtered heap kernel over queries qq, rows into (oi, od)
+        auto launch_heaps = [&](const Queries& qq, i64 sb, u32* oi, double* od) {
+            const int hb = grid_for(qq.m);
+            const u32 seed_half = std::max<u32>(16, kh);
+            u64* counter = dalloc_t<u64>(ctx, 1);
+            LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
+            if (global_heap) {
+                if (!gk) {
+                    gk = dalloc_t<float>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
+                    gi = dalloc_t<u32>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
+                }
+                LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<true, 0, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                knn_float_kernel<true, 0, true><<<std::min(hb, blocks), 32 * warps, smem, ctx->stream>>>(
+                    t->tf, c->pf, c->x, c->y, c->z, c->n, qq, sb, seed_half, E, kh, oi, od, gk, gi, counter);
+            } else {
+                // common k compile to fixed-depth, unrolled heap sifts
+#define LO_KNN_LAUNCH(KC, KEYED)                                                                          \
+    do {                                                                                                  \
+        LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<false, KC, KEYED>,                                  \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));\
+        knn_float_kernel<false, KC, KEYED><<<hb, 32 * warps, smem, ctx->stream>>>(                        \
+            t->tf, c->pf, c->x, c->y, c->z, c->n, qq, sb, seed_half, E, kh, oi, od, nullptr, nullptr,     \
+            counter);                                                                                     \
+    } while (0)
+                switch (kh) {
+                    case 8: LO_KNN_LAUNCH(8, false); break;
+                    case 16: LO_KNN_LAUNCH(16, false); break;
+                    case 32: LO_KNN_LAUNCH(32, true); break;
+                    case 64: LO_KNN_LAUNCH(64, true); break;
+                    default:
+                        if (keyed) LO_KNN_LAUNCH(0, true);
+                        else LO_KNN_LAUNCH(0, false);
+                        break;
+                }
+#undef LO_KNN_LAUNCH
+            }
+            LO_CHECK_LAUNCH();
+            dfree(ctx, counter);
+        };
         stage_begin(ctx, "knn");
         // LO_KNN_WARP=1: the warp-cooperative kernel (knn_warp.cuh, k <= 64).  Exact, but measured 4-6x
         // slower than the per-lane heaps (cfg1 k = 8/16/32/64: 31.9/44.6/120/386 vs 6.6/11.0/21.6/59.6 ms):
@@ -411,9 +458,10 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
         // ~k candidates to each of the 32 queries one query at a time (the per-lane heaps take them in
         // parallel).  Kept as the measured alternative; DESIGN.md §8.
         const bool warp_kernel = use_float && kh <= 64 && env_flag("LO_KNN_WARP");
+        // LO_KNN_SELECT=1: candidate collection + warp selection (knn_select.cuh) for batches of cloud
+        // points (Full / range / centre lists)
+        const bool select_path = use_float && kh <= 64 && seed_base != -1 && env_flag("LO_KNN_SELECT");
         if (q.m && warp_kernel) {
-            float E = static_cast<float>(std::ldexp(std::max(c->bmax, q.bmax), -23));
-            E = std::nextafter(E, INFINITY);  // round up
             const u32 seed_half = std::max<u32>(16, kh);
             const size_t per_warp = knn_warp_smem_per_warp(kh);
             const size_t wsmem = kKwWarps * per_warp;
@@ -433,44 +481,10 @@ static lo_knn_result* knn_search(lo_context* ctx, const lo_octree* t, const lo_c
             }
             LO_CHECK_LAUNCH();
             dfree(ctx, counter);
+        } else if (q.m && select_path) {
+            knn_select_run(ctx, t, c, q, kh, seed_base, E, out->idx, out->dist, launch_heaps);
         } else if (q.m && use_float) {
-            float E = static_cast<float>(std::ldexp(std::max(c->bmax, q.bmax), -23));
-            E = std::nextafter(E, INFINITY);  // round up
-            const u32 seed_half = std::max<u32>(16, kh);
-            u64* counter = dalloc_t<u64>(ctx, 1);
-            LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
-            if (global_heap) {
-                gk = dalloc_t<float>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
-                gi = dalloc_t<u32>(ctx, static_cast<u64>(blocks) * warps * kh * 32);
-                LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<true, 0, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                knn_float_kernel<true, 0, true><<<blocks, 32 * warps, smem, ctx->stream>>>(
-                    t->tf, c->pf, c->x, c->y, c->z, c->n, q, seed_base, seed_half, E, kh, out->idx,
-                    out->dist, gk, gi, counter);
-            } else {
-                // common k compile to fixed-depth, unrolled heap sifts
-#define LO_KNN_LAUNCH(KC, KEYED)                                                                          \
-    do {                                                                                                  \
-        LO_CUDA(cudaFuncSetAttribute(knn_float_kernel<false, KC, KEYED>,                                  \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));\
-        knn_float_kernel<false, KC, KEYED><<<blocks, 32 * warps, smem, ctx->stream>>>(                    \
-            t->tf, c->pf, c->x, c->y, c->z, c->n, q, seed_base, seed_half, E, kh, out->idx, out->dist,    \
-            nullptr, nullptr, counter);                                                                   \
-    } while (0)
-                switch (kh) {
-                    case 8: LO_KNN_LAUNCH(8, false); break;
-                    case 16: LO_KNN_LAUNCH(16, false); break;
-                    case 32: LO_KNN_LAUNCH(32, true); break;
-                    case 64: LO_KNN_LAUNCH(64, true); break;
-                    default:
-                        if (keyed) LO_KNN_LAUNCH(0, true);
-                        else LO_KNN_LAUNCH(0, false);
-                        break;
-                }
-#undef LO_KNN_LAUNCH
-            }
-            LO_CHECK_LAUNCH();
-            dfree(ctx, counter);
+            launch_heaps(q, seed_base, out->idx, out->dist);
         } else if (q.m) {
             if (global_heap) {
                 gd = dalloc_t<double>(ctx, static_cast<u64>(blocks) * warps * kh * 32);

@@ -7,7 +7,9 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -15,6 +17,7 @@
 #include <string>
 #include <atomic>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/linoct_b200.h"
@@ -109,6 +112,7 @@ struct lo_context {
     void* pinned_scratch_dev = nullptr; // its device alias
     void* arena = nullptr;              // persistent device scratch (radius records)
     size_t arena_bytes = 0;
+    uint64_t arena_budgeted = 0;  // record demand (bytes) the arena was last sized for under the free-memory cap
     // asynchronous result downloads (lo_csr_download_async): D2H on a second stream so the
     // next batch computes while the previous one's results travel; buffers of results destroyed
     // while their copy is in flight are released once the copy has completed.
@@ -132,6 +136,9 @@ struct lo_context {
         cudaEvent_t ready;
     };
     std::vector<Cached> cache;
+    std::unordered_map<void*, size_t> big;  // live buffers handed out from (and parked back to) the cache
+    size_t cache_cap = 0;                   // parked-bytes cap (a quarter of the device memory)
+    cudaEvent_t sync_ev = nullptr;          // sync(): recorded, then spun on (no sleeping wait)
     static constexpr int kH2dSlots = 4;
     cudaEvent_t h2d_done[kH2dSlots] = {};
     cudaEvent_t d2h_done[kH2dSlots] = {};  // lo_d2h_fence / lo_d2h_wait
@@ -315,6 +322,7 @@ void* arena(lo_context* ctx, size_t bytes);
 void stage_begin(lo_context* ctx, const char* name);
 void stage_end(lo_context* ctx);
 void sync(lo_context* ctx);
+void spin_wait(cudaEvent_t ev);  // busy-waits for a recorded event
 // Copies `bytes` (<= 16384, 4-byte aligned) of device memory into ctx->pinned_scratch and waits.
 // A one-warp kernel stores them through the mapped alias instead of a cudaMemcpy: a D2H copy on
 // the context stream queued behind the copy engine's pending result downloads (lo_csr_download_async
@@ -482,10 +490,32 @@ inline int ceil_div(u64 a, u64 b) { return static_cast<int>((a + b - 1) / b); }
 //                        radii below ~2.4e-5 x the cube side take on their own
 //   LO_RADIUS_NO_FUSE=1  radius fill by a second walk instead of replaying count-pass records
 //   LO_REC_CAP=<n>       records per tile before a tile overflows to the fill walk (default 128)
+//   LO_KNN_SELECT=1      kNN by candidate collection + warp selection (knn_select.cuh), with
+//                        LO_KNN_WIN / LO_KNN_CAP / LO_KNN_LIST_MB (bound window, list capacity, chunk)
+//   LO_KNN_WARP=1        kNN by the warp-cooperative heaps (knn_warp.cuh)
 inline bool env_flag(const char* name) {
     const char* e = std::getenv(name);
     return e && *e && *e != '0';
 }
 inline bool force_fp64() { return env_flag("LO_FORCE_FP64"); }
+
+// LO_DEBUG_HOST=1 (diagnostic): host calls of the library that take over 1 ms are logged to stderr
+struct SlowLog {
+    const char* what;
+    size_t arg;
+    std::chrono::steady_clock::time_point t0;
+    static bool on() {
+        static const bool enabled = std::getenv("LO_DEBUG_HOST") != nullptr;
+        return enabled;
+    }
+    SlowLog(const char* w, size_t a) : what(w), arg(a) {
+        if (on()) t0 = std::chrono::steady_clock::now();
+    }
+    ~SlowLog() {
+        if (!on()) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms > 1.0) std::fprintf(stderr, "[lo] slow host call %s(%zu): %.2f ms\n", what, arg, ms);
+    }
+};
 
 }  // namespace lo

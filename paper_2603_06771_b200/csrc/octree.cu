@@ -299,12 +299,14 @@ void ensure_float_shadows(lo_context* ctx, const lo_coded* coded, const lo_octre
     {
         std::lock_guard<std::mutex> g(c->lazy_mu);
         if (!c->pf) {
+            SlowLog slow("float points", c->n);
             build_float_points(ctx, c);
             sync(ctx);
         }
     }
     std::lock_guard<std::mutex> g(t->lazy_mu);
     if (!t->tf) {
+        SlowLog slow("float nodes", 0);
         build_float_nodes(ctx, t, coded);
         sync(ctx);
     }

@@ -8,6 +8,7 @@
 // leaf points are staged in shared memory and tested by every intersecting lane with the
 // exact predicate.  DFS visits children in code order, so rows come out ascending like the
 // reference's.
+#include <chrono>
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -225,13 +226,26 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
     out->ctx = ctx;
     out->rows = q.m;
     cudaEvent_t e0, e1;
-    LO_CUDA(cudaEventCreate(&e0));
-    LO_CUDA(cudaEventCreate(&e1));
+    {
+        SlowLog slow("radius event create", 0);
+        LO_CUDA(cudaEventCreate(&e0));
+        LO_CUDA(cudaEventCreate(&e1));
+    }
     RecArgs ra;
     u32* ovf = nullptr;
     u32* ovf_n = nullptr;
+    // LO_DEBUG_HOST=1: host time of each segment of the call, printed for slow calls (diagnostic)
+    static const bool dbg_host = std::getenv("LO_DEBUG_HOST") != nullptr;
+    using clk = std::chrono::steady_clock;
+    clk::time_point tm[8];
+    int ntm = 0;
+    const auto mark = [&] { if (dbg_host) tm[ntm++] = clk::now(); };
     try {
-        LO_CUDA(cudaEventRecord(e0, ctx->stream));
+        mark();
+        {
+            SlowLog slow("radius events", 0);
+            LO_CUDA(cudaEventRecord(e0, ctx->stream));
+        }
         out->counts = big_alloc_t<u32>(ctx, q.m, &out->cap[0]);
         out->offsets = big_alloc_t<u64>(ctx, q.m + 1, &out->cap[2]);
         const u64 tiles = (q.m + 31) / 32;
@@ -256,13 +270,17 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
         u64* fused_fps = fingerprint && env_flag("LO_DIGEST_FUSED") ? out->fps : nullptr;
         stage_begin(ctx, "radius_count");
         bool digested = false;
+        mark();
         if (q.m) digested = launch_radius<false>(ctx, shape, t, c, q, r, out->counts, nullptr, nullptr, ra, fused_fps);
         stage_end(ctx);
         stage_begin(ctx, "radius_scan");
         exclusive_scan_u32_to_u64(ctx, out->counts, out->offsets, q.m);
         stage_end(ctx);
+        mark();
         out->total = read_scalar(ctx, out->offsets + q.m);
+        mark();
         out->indices = big_alloc_t<u32>(ctx, out->total, &out->cap[3]);
+        mark();
         stage_begin(ctx, "radius_fill");
         if (q.m && ra.rp.pool) {
             const u32 n_ovf = replay_records(ctx, RecSetup{ra.rp, ovf, ovf_n}, q.m, out->offsets,
@@ -313,8 +331,19 @@ static lo_csr* radius_search(lo_context* ctx, const lo_octree* t, const lo_coded
                 LO_CUDA(cudaEventRecord(e1, ctx->stream));
             }
         }
-        LO_CUDA(cudaEventSynchronize(e1));
+        mark();
+        spin_wait(e1);
+        mark();
         LO_CUDA(cudaEventElapsedTime(&out->ms, e0, e1));
+        if (dbg_host) {
+            const double tot = std::chrono::duration<double, std::milli>(tm[ntm - 1] - tm[0]).count();
+            {
+                std::fprintf(stderr, "[lo] radius call %.2f ms host, %.2f ms device; segments:", tot, out->ms);
+                for (int i = 1; i < ntm; ++i)
+                    std::fprintf(stderr, " %.2f", std::chrono::duration<double, std::milli>(tm[i] - tm[i - 1]).count());
+                std::fprintf(stderr, "\n");
+            }
+        }
         out->mean = q.m ? static_cast<double>(out->total) / static_cast<double>(q.m) : 0.0;
     } catch (...) {
         free_csr_buffers(ctx, out);

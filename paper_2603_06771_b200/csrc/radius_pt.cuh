@@ -394,16 +394,23 @@ struct RecSetup {
     u32* ovf_n = nullptr;
 };
 static inline RecSetup setup_records(lo_context* ctx, u64 tiles, u32 cap) {
+    SlowLog slow("setup_records", tiles);
     RecSetup rs;
     const u64 head = 8 * (tiles + 1) + 4 * (2 * tiles + 1);
     u64 recs = tiles * cap;
-    if (head + 16 + recs * 256 > ctx->arena_bytes) {  // growing: respect free memory
+    const u64 demand = head + 16 + recs * 256;
+    // cudaMemGetInfo is queried only when the demand outgrows what the arena was last budgeted for:
+    // it blocked the host for 2-70 ms at random while the GPU was busy, idling the device mid-step
+    const bool reuse = demand <= ctx->arena_bytes ||
+                       (demand <= ctx->arena_budgeted && ctx->arena_bytes >= head + 16 + 2 * kRecChunk * 256);
+    if (reuse) {  // whatever the arena holds
+        recs = (ctx->arena_bytes - head - 16) / 256;
+    } else {  // growing: respect free memory
         size_t free_b = 0, total_b = 0;
         LO_CUDA(cudaMemGetInfo(&free_b, &total_b));
         const u64 budget = (free_b + ctx->arena_bytes) / 4;
         recs = std::min<u64>(recs, budget > head ? (budget - head) / 256 : 0);
-    } else {  // reuse whatever the arena holds
-        recs = (ctx->arena_bytes - head - 16) / 256;
+        ctx->arena_budgeted = demand;
     }
     recs = std::max<u64>(recs, kRecChunk * 2);
     unsigned char* base = static_cast<unsigned char*>(arena(ctx, head + 16 + recs * 256));

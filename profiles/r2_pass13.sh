@@ -1,0 +1,6 @@
+#!/bin/bash
+OUT=gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 600 python profiles/gap_probe.py --config cfg3 --steps 8 > $OUT/gap13.log 2>&1
+timeout 600 python profiles/gap_probe.py --config cfg1 --steps 16 >> $OUT/gap13.log 2>&1
+exit 0

@@ -1,0 +1,5 @@
+#!/bin/bash
+OUT=gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 900 python profiles/gap_probe.py --config cfg3 --steps 8 > $OUT/gap14.log 2>&1
+exit 0

@@ -1,0 +1,5 @@
+#!/bin/bash
+OUT=gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+LO_DEBUG_ALLOC=1 timeout 900 python profiles/step_var_probe.py --config cfg3 --steps 12 > $OUT/var17.log 2> $OUT/var17.err
+exit 0

@@ -127,20 +127,48 @@ def test_fused_digest_pass(ctx, ref, oracle, monkeypatch):
         monkeypatch.delenv("LO_DIGEST_FUSED")
 
 
-@pytest.mark.parametrize("warp", ["0", "1"])
-def test_knn_kernels_k_up_to_64(ctx, ref, oracle, monkeypatch, warp):
-    """The per-lane-heap kNN kernel (default) and, with LO_KNN_WARP=1, the warp-cooperative one
-    (knn_warp.cuh, k <= 64).  Full mode and RandomSubset (per-query seed windows)."""
+KNN_VARIANTS = {
+    "select": {"LO_KNN_SELECT": "1"},                        # bound + collect + warp select
+    "select_overflow": {"LO_KNN_SELECT": "1", "LO_KNN_CAP": "1", "LO_KNN_WIN": "1"},  # 32-entry lists
+    "select_chunked": {"LO_KNN_SELECT": "1", "LO_KNN_LIST_MB": "1"},  # 32k-query chunks
+    "heaps": {"LO_KNN_SELECT": "0"},                         # per-lane heaps (knn_float.cuh, default)
+    "warp": {"LO_KNN_WARP": "1"},                            # warp-cooperative heaps (knn_warp.cuh)
+}
+
+
+@pytest.mark.parametrize("variant", sorted(KNN_VARIANTS))
+def test_knn_kernels_k_up_to_64(ctx, ref, oracle, monkeypatch, variant):
+    """Every kNN kernel path for k <= 64: the candidate-selection path (knn_select.cuh),
+    with most queries overflowing into the heap fallback, in small chunks, the per-lane heaps and
+    the warp-cooperative heaps.  Full mode and RandomSubset (per-query seed windows)."""
     pts = oracle.gen_mixed(70_000, 17)
     p = ref.pipeline(pts, 1, 64)
     coded, tree = pipeline(pts, 1, 64)
-    monkeypatch.setenv("LO_KNN_WARP", warp)
+    for key, val in KNN_VARIANTS[variant].items():
+        monkeypatch.setenv(key, val)
     for k in (1, 2, 8, 16, 31, 32, 33, 48, 64):
         check_knn(tree, coded, p, k)
         want = p.knn(k, mode=1, subset=3000, seed=k)
         got = lo.run_knn_batch(tree, coded, k, lo.BatchOptions(mode=lo.BatchMode.RandomSubset, subset_size=3000,
                                                                seed=k))
         assert np.array_equal(got.fingerprints, want["fps"]), k
+
+
+@pytest.mark.parametrize("jitter", [0.0, 1e-9])
+def test_knn_select_ties(ctx, ref, monkeypatch, jitter):
+    """A lattice: many candidates at exactly equal distances (order by index) or, with a 1e-9
+    jitter, at distances equal in their FP32 round-up but not in FP64 (the selection re-sorts those
+    runs by the exact (dist_sq, index))."""
+    g = np.arange(36, dtype=np.float64)
+    pts = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3) + 100.0
+    if jitter:
+        pts = pts + np.random.default_rng(5).uniform(-jitter, jitter, pts.shape)
+    p = ref.pipeline(pts, 1, 32)
+    coded, tree = pipeline(pts, 1, 32)
+    for sel in ("1", "0"):
+        monkeypatch.setenv("LO_KNN_SELECT", sel)
+        for k in (7, 8, 19, 27, 33, 64):
+            check_knn(tree, coded, p, k)
 
 
 def test_knobs_off_again(ctx, ref, oracle):
