@@ -712,9 +712,12 @@ void free_csr_buffers(lo_context* ctx, lo_csr* csr) {
     };
     cudaStream_t last = ctx->stream;
     unsigned guarded = 0;
+    const bool aux_digests = csr->digested != nullptr;
     if (pending(csr->copied)) {
         last = ctx->copy_stream;
-        guarded = csr->copy_mask | 2u | 4u | 8u;  // the copy stream also waited for the digests
+        // the copied buffers, and with aux-stream digests also what the digests read (the copy
+        // stream waited for them); inline digests finished on ctx->stream already
+        guarded = csr->copy_mask | (aux_digests ? 2u | 4u | 8u : 0u);
     }
     if (pending(csr->digested) && !guarded) {
         last = ctx->aux_stream;
