@@ -493,6 +493,9 @@ inline int ceil_div(u64 a, u64 b) { return static_cast<int>((a + b - 1) / b); }
 //   LO_KNN_SELECT=1      kNN by candidate collection + warp selection (knn_select.cuh), with
 //                        LO_KNN_WIN / LO_KNN_CAP / LO_KNN_LIST_MB (bound window, list capacity, chunk)
 //   LO_KNN_WARP=1        kNN by the warp-cooperative heaps (knn_warp.cuh)
+// Diagnostics (read once): LO_DEBUG=1 (arena growth, record overflow, kNN select chunks),
+// LO_DEBUG_ALLOC=1 (slow cudaMallocAsync calls), LO_DEBUG_HOST=1 (host calls over 1 ms, and the host
+// segments of every radius call).
 inline bool env_flag(const char* name) {
     const char* e = std::getenv(name);
     return e && *e && *e != '0';
