@@ -1,6 +1,12 @@
 """Randomised parity sweep (seeded, deterministic): many small clouds with random shape, size,
 level, curve, leaf bucket, kernel shape, radius, k and query mode, each checked against the C
-restatement (brute-force radius / kNN, the Struct traversal) -- bit for bit."""
+restatement (brute-force radius / kNN, the Struct traversal) -- bit for bit.  A second sweep runs
+mid-size clouds (50k-400k points) through the reference library itself (oracle/_ref, Full mode:
+every point a centre, counts + FNV digests of every row, kNN digests).
+
+LO_FUZZ_CASES / LO_FUZZ_REF_CASES scale the sweeps (defaults 120 / 8) for longer campaigns."""
+import os
+
 import numpy as np
 import pytest
 
@@ -36,7 +42,7 @@ def cloud(rng, kind, n):
     return p
 
 
-@pytest.mark.parametrize("case", range(120))
+@pytest.mark.parametrize("case", range(int(os.environ.get("LO_FUZZ_CASES", "120"))))
 def test_fuzz_against_oracle(ctx, oracle, case):
     rng = np.random.default_rng(1000 + case)
     kind = ["uniform", "clusters", "coincident", "grid", "flat"][case % 5]
@@ -90,3 +96,44 @@ def test_fuzz_against_oracle(ctx, oracle, case):
     rows = lo.radius_points(tree, coded, lo.KernelShape(shape), r, off)
     for j, c in enumerate(off):
         assert np.array_equal(rows[j], oracle.radius_brute(xs, c, r, shape))
+
+
+def midsize_cloud(rng, oracle, kind, n):
+    seed = int(rng.integers(1, 1 << 30))
+    if kind == "uniform":
+        return oracle.gen_uniform(n, seed, float(rng.choice([10.0, 100.0, 1000.0])))
+    if kind == "terrain":
+        return oracle.gen_terrain(n, seed, float(rng.choice([100.0, 300.0, 1000.0])))
+    if kind == "mixed":
+        return oracle.gen_mixed(n, seed)
+    # dense clusters in a large empty cube (sparse tiles, long curve jumps)
+    c = rng.random((max(1, n // 2000), 3)) * 5000.0
+    return c[rng.integers(0, len(c), n)] + rng.normal(0, float(rng.choice([0.3, 2.0])), (n, 3))
+
+
+@pytest.mark.parametrize("case", range(int(os.environ.get("LO_FUZZ_REF_CASES", "8"))))
+def test_fuzz_midsize_against_reference(ctx, oracle, ref, case):
+    rng = np.random.default_rng(77_000 + case)
+    kind = ["uniform", "terrain", "mixed", "clusters"][case % 4]
+    n = int(rng.integers(50_000, 400_000))
+    pts = midsize_cloud(rng, oracle, kind, n)
+    curve = int(rng.integers(0, 2))
+    n_max = int(rng.choice([8, 32, 64, 200]))
+    p = ref.pipeline(pts, curve, n_max)
+    coded = lo.reorder_cloud(pts, lo.Curve(curve))
+    tree = lo.LinearOctree(coded, n_max)
+    # a radius that gives ~mu neighbours on average: from the k-th neighbour distance of a sample
+    from scipy.spatial import cKDTree
+    mu = int(rng.choice([4, 16, 64, 200]))
+    xs = coded.cloud.points
+    d, _ = cKDTree(xs).query(xs[rng.integers(0, len(xs), 256)], k=mu + 1)
+    r = float(np.median(d[:, -1])) or 1.0
+    shape = int(rng.integers(0, 4))
+    want = p.radius(r, shape=shape)
+    got = lo.run_radius_batch(tree, coded, lo.RadiusMethod.Lin, lo.KernelShape(shape), r, lo.BatchOptions())
+    assert np.array_equal(got.counts, want["counts"]), (kind, n, curve, n_max, shape, r)
+    assert np.array_equal(got.fingerprints, want["fps"]), (kind, n, curve, n_max, shape, r)
+    k = int(rng.choice([1, 8, 16, 32, 64]))
+    kw = p.knn(k)
+    kg = lo.run_knn_batch(tree, coded, k, lo.BatchOptions())
+    assert np.array_equal(kg.fingerprints, kw["fps"]), (kind, n, curve, n_max, k)
