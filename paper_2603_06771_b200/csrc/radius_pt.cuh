@@ -23,6 +23,9 @@
 namespace lo {
 
 constexpr int kPtWarps = 4;
+#ifndef LO_PT_PREFILTER
+#define LO_PT_PREFILTER 1
+#endif
 constexpr int kPtThreads = 32 * kPtWarps;
 
 struct PtShared {
@@ -616,6 +619,17 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             }
         }
         const bool gcompact = fmaxf(fmaxf(gh[0] - gl[0], gh[1] - gl[1]), gh[2] - gl[2]) <= compact;
+        // the whole tile's query box: candidate points farther than r from it are members of no
+        // query of the tile (tile_disjoint_f with the point as a degenerate box), so they are
+        // dropped before they take a buffer slot
+        float tl[3], th[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            tl[a] = fminf(gl[a], __shfl_xor_sync(~0u, gl[a], 8));
+            th[a] = fmaxf(gh[a], __shfl_xor_sync(~0u, gh[a], 8));
+            tl[a] = fminf(tl[a], __shfl_xor_sync(~0u, tl[a], 16));
+            th[a] = fmaxf(th[a], __shfl_xor_sync(~0u, th[a], 16));
+        }
         u32 fill = 0, qmask = 0;  // buffer occupancy and interested queries (warp-uniform)
         u32 nrec = 0;             // count pass: buffers recorded for the replay
         u64 hash = kFnvOffset;    // DIGEST: row L's FNV-1a-64 so far
@@ -681,6 +695,37 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             // leaf: which queries can reach it
             const u32 want = __ballot_sync(~0u, active && !disjoint_f<SHAPE>(qf, nd, ft));
             if (!want) continue;
+#if LO_PT_PREFILTER
+            for (u32 b0 = nd.begin; b0 < nd.end; b0 += 32) {
+                const u32 g = b0 + static_cast<u32>(lane);
+                bool ok = false;
+                if (g < nd.end) {
+                    const float4 pp = __ldg(pf + g);
+                    NodeF pt;
+                    pt.lo[0] = pt.hi[0] = pp.x;
+                    pt.lo[1] = pt.hi[1] = pp.y;
+                    pt.lo[2] = pt.hi[2] = pp.z;
+                    ok = !tile_disjoint_f<SHAPE>(tl, th, pt, ft);
+                }
+                const u32 bal = __ballot_sync(~0u, ok);
+                if (!bal) continue;
+                const u32 pos = fill + __popc(bal & ((1u << lane) - 1u));
+                __syncwarp();
+                if (ok && pos < 32) S.bix[pos] = g;
+                fill += __popc(bal);
+                qmask |= want;
+                if (fill >= 32) {
+                    const u32 over = fill - 32;
+                    fill = 32;
+                    __syncwarp();
+                    flush();
+                    __syncwarp();
+                    if (ok && pos >= 32) S.bix[pos - 32] = g;
+                    fill = over;
+                    qmask = over ? want : 0u;
+                }
+            }
+#else
             for (u32 base = nd.begin; base < nd.end;) {
                 const u32 take = min(32u - fill, nd.end - base);
                 __syncwarp();
@@ -695,6 +740,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
                     qmask = 0;
                 }
             }
+#endif
         }
         if (fill) {
             __syncwarp();

@@ -149,30 +149,45 @@ __global__ void __launch_bounds__(256) encode_kernel(const double* __restrict__ 
 }
 
 // ---- K3: onesweep LSD radix sort pass (8-bit digit, stable, decoupled look-back) ---------
-// Tile = 256 threads x 16 keys.  Each warp ranks its 512 keys round by round (lane order
-// within a round, round order within the warp) with __match_any_sync, which keeps equal
-// digits in input order; tiles chain their per-digit totals through a look-back status
-// array (flag in the top 2 bits of a u64 word), so each pass reads and writes every
-// (key, value) exactly once.
+// Tile = 256 threads x kSortItems keys; warp w owns keys [w*32*I, (w+1)*32*I) in (item, lane)
+// order.  Each warp ranks its keys with __match_any_sync; the per-item running counts go through
+// one shared-memory atomic per distinct digit, issued back to back (a warp's shared atomics
+// execute in program order, so equal digits keep input order) instead of a load / store /
+// __syncwarp chain per item.  Tiles chain their per-digit totals through a look-back status word
+// per (tile, digit): flag (2 bits) | pass epoch (6 bits) | count (56 bits), so one memset per sort
+// serves every pass.  Order inside a tile: (1) ranking, (2) local offsets and the tile's
+// aggregate published, (3) the tile is scattered into shared memory and its values loaded,
+// (4) only then the look-back for the global digit prefix (predecessors had the scatter's time to
+// publish), (5) coalesced global writes.  cfg3 sort 9.04 -> 7.46 ms, cfg1 1.124 -> 1.027 ms
+// (torch.sort / CUB SortPairs on the same counts of 64-bit keys: 8.61 / 1.03 ms,
+// profiles/r3/sort_v2.log).  LO_SORT_EARLY=1 publishes an early block histogram (shared
+// atomics) before the ranking instead; measured slower (8.09 / 1.073 ms).
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-// 12 keys per thread, 4 blocks per SM (48 KB of shared memory each): cfg3 sort 9.50 -> 8.85 ms,
-// cfg1 1.145 -> 1.023 ms against 16 / 3 (8 / 5: 10.18 / 1.089; 16 / 4: 9.35 / 1.111; sort_probe.py)
 #ifndef LO_SORT_ITEMS
 #define LO_SORT_ITEMS 12
 #endif
 #ifndef LO_SORT_MINB
 #define LO_SORT_MINB 4
 #endif
+#ifndef LO_SORT_EARLY
+#define LO_SORT_EARLY 0
+#endif
+#ifndef LO_SORT_GROUP
+#define LO_SORT_GROUP 4
+#endif
 constexpr int kSortItems = LO_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr u64 kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kFlagMask = 3ull << 62;
+constexpr int kEpochShift = 56;
+constexpr u64 kCountMask = (1ull << kEpochShift) - 1;
 
 struct SortSmem {
     u64 keys[kSortTile];
     u32 vals[kSortTile];
     u32 whist[kSortWarps][256];
     u32 local_start[256];
+    u32 bhist[256];
     u64 gofs[256];
     u32 tile;
     typename cub::BlockScan<u32, kSortThreads>::TempStorage scan;
@@ -182,42 +197,61 @@ template <bool FIRST>
 __global__ void __launch_bounds__(kSortThreads, LO_SORT_MINB) onesweep_pass(
     const u64* __restrict__ kin, const u32* __restrict__ vin, u64* __restrict__ kout,
     u32* __restrict__ vout, u64 n, int shift, const u64* __restrict__ digit_base,
-    u64* status, u32* counter) {
+    u64* status, u32* counter, u32 epoch) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     if (tid == 0) S.tile = atomicAdd(counter, 1u);
     for (int i = tid; i < kSortWarps * 256; i += kSortThreads) (&S.whist[0][0])[i] = 0;
+    if (LO_SORT_EARLY) S.bhist[tid] = 0;
     __syncthreads();
     const u32 tile = S.tile;
     const u64 base = static_cast<u64>(tile) * kSortTile;
     const u64 wbase = base + static_cast<u64>(w) * (32 * kSortItems);
+    const u64 ep = static_cast<u64>(epoch) << kEpochShift;
+    volatile u64* st = status + static_cast<u64>(tile) * 256;
 
     u64 key[kSortItems];
     u32 rank[kSortItems];
 #pragma unroll
     for (int i = 0; i < kSortItems; ++i) {
         const u64 idx = wbase + i * 32 + lane;
-        key[i] = idx < n ? kin[idx] : 0ull;
+        key[i] = idx < n ? kin[idx] : ~0ull;  // pad keys: digit 255, ranked last
     }
+    const u64 tile_n = min(static_cast<u64>(kSortTile), n - base);
+    if (LO_SORT_EARLY) {
+        // early block histogram, so successors see this tile's aggregate while it ranks
+#pragma unroll
+        for (int i = 0; i < kSortItems; ++i)
+            if (wbase + i * 32 + lane < n) atomicAdd(&S.bhist[(key[i] >> shift) & 0xff], 1u);
+        __syncthreads();
+        st[tid] = (tile == 0 ? kFlagInc : kFlagAgg) | ep | S.bhist[tid];
+    }
+    // (1) ranking: match a group of items, then one leader atomic per distinct digit and item
+    constexpr int G = LO_SORT_GROUP;
+    static_assert(kSortItems % G == 0, "items per thread must be a multiple of the match group");
     const u32 lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
-        const bool valid = wbase + i * 32 + lane < n;
-        const u32 d = valid ? static_cast<u32>((key[i] >> shift) & 0xff) : 256u + lane;
-        const u32 peers = __match_any_sync(~0u, d);
-        u32 cnt = 0;
-        if (valid) {
-            cnt = S.whist[w][d];
-            rank[i] = cnt + __popc(peers & lt);
+    for (int i0 = 0; i0 < kSortItems; i0 += G) {
+        u32 peers[G], old[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            const u32 d = static_cast<u32>((key[i0 + u] >> shift) & 0xff);
+            peers[u] = __match_any_sync(~0u, d);
         }
-        __syncwarp();
-        if (valid && lane == __ffs(peers) - 1) S.whist[w][d] = cnt + __popc(peers);
-        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            const u32 d = static_cast<u32>((key[i0 + u] >> shift) & 0xff);
+            old[u] = 0;
+            if (lane == __ffs(peers[u]) - 1) old[u] = atomicAdd(&S.whist[w][d], static_cast<u32>(__popc(peers[u])));
+        }
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+            rank[i0 + u] = __shfl_sync(~0u, old[u], __ffs(peers[u]) - 1) + __popc(peers[u] & lt);
     }
     __syncthreads();
 
-    // per digit: exclusive offsets across warps, tile total, look-back for the global prefix
+    // (2) per digit: exclusive offsets across warps, tile total, local starts
     const int d = tid;
     u32 total = 0;
 #pragma unroll
@@ -226,46 +260,54 @@ __global__ void __launch_bounds__(kSortThreads, LO_SORT_MINB) onesweep_pass(
         S.whist[ww][d] = total;
         total += c;
     }
-    volatile u64* st = status;
-    st[static_cast<u64>(tile) * 256 + d] = (tile == 0 ? kFlagInc : kFlagAgg) | total;
-    u64 excl = 0;
-    if (tile > 0) {
-        i64 j = static_cast<i64>(tile) - 1;
-        for (;;) {
-            const u64 s = st[static_cast<u64>(j) * 256 + d];
-            const u64 f = s & kFlagMask;
-            if (f == 0) continue;
-            excl += s & ~kFlagMask;
-            if (f == kFlagInc) break;
-            --j;
-        }
-        st[static_cast<u64>(tile) * 256 + d] = kFlagInc | (excl + total);
-    }
-    S.gofs[d] = digit_base[d] + excl;
+    // pad keys sit at the top of digit 255: drop them from the published count
+    const u32 pad = static_cast<u32>(kSortTile - tile_n);
+    const u32 real = d == 255 ? total - pad : total;
+    if (!LO_SORT_EARLY) st[d] = (tile == 0 ? kFlagInc : kFlagAgg) | ep | real;
     u32 lstart;
     cub::BlockScan<u32, kSortThreads>(S.scan).ExclusiveSum(total, lstart);
     S.local_start[d] = lstart;
     __syncthreads();
 
+    // (3) scatter the tile into shared memory in digit order; load the values meanwhile
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+        const u32 dd = static_cast<u32>((key[i] >> shift) & 0xff);
+        const u32 pos = S.local_start[dd] + S.whist[w][dd] + rank[i];
+        S.keys[pos] = key[i];
+        rank[i] = pos;
+    }
 #pragma unroll
     for (int i = 0; i < kSortItems; ++i) {
         const u64 idx = wbase + i * 32 + lane;
-        if (idx < n) {
-            const u32 dd = static_cast<u32>((key[i] >> shift) & 0xff);
-            const u32 pos = S.local_start[dd] + S.whist[w][dd] + rank[i];
-            S.keys[pos] = key[i];
-            S.vals[pos] = FIRST ? static_cast<u32>(idx) : vin[idx];
-        }
+        const u32 v = FIRST ? static_cast<u32>(idx) : (idx < n ? vin[idx] : 0u);
+        S.vals[rank[i]] = v;
     }
+
+    // (4) look back for this digit's global prefix
+    u64 excl = 0;
+    if (tile > 0) {
+        volatile u64* sp = status + static_cast<u64>(tile - 1) * 256 + d;
+        for (;;) {
+            const u64 s = *sp;
+            const u64 f = s & kFlagMask;
+            if (f == 0 || (s & ~kFlagMask) >> kEpochShift != epoch) continue;
+            excl += s & kCountMask;
+            if (f == kFlagInc) break;
+            sp -= 256;
+        }
+        st[d] = kFlagInc | ep | (excl + real);
+    }
+    S.gofs[d] = digit_base[d] + excl - lstart;
     __syncthreads();
-    const u64 tile_n = min(static_cast<u64>(kSortTile), n - base);
+
+    // (5) coalesced global writes: consecutive threads write consecutive slots of a digit run
 #pragma unroll
     for (int i = 0; i < kSortItems; ++i) {
         const u32 p = i * kSortThreads + tid;
         if (p < tile_n) {
             const u64 k = S.keys[p];
-            const u32 dd = static_cast<u32>((k >> shift) & 0xff);
-            const u64 gp = S.gofs[dd] + (p - S.local_start[dd]);
+            const u64 gp = S.gofs[(k >> shift) & 0xff] + p;
             kout[gp] = k;
             vout[gp] = S.vals[p];
         }
@@ -498,7 +540,9 @@ void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int lev
         LO_CUDA(cudaMemcpyAsync(dbase, bases.data(), bases.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
     }
     u64* status = dalloc_t<u64>(ctx, static_cast<size_t>(tiles) * 256);
-    u32* counter = dalloc_t<u32>(ctx, 1);
+    u32* counter = dalloc_t<u32>(ctx, 8);
+    // one status memset per sort: each pass tags its words with its own epoch (i + 1)
+    LO_CUDA(cudaMemsetAsync(status, 0, static_cast<size_t>(tiles) * 256 * 8, ctx->stream));
     u64* kalt = dalloc_t<u64>(ctx, n);
     u32* valt = dalloc_t<u32>(ctx, n);
     u32* vtmp = dalloc_t<u32>(ctx, n);
@@ -517,14 +561,13 @@ void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int lev
         const bool last = i == np - 1;
         u64* kout = last ? keys_sorted : (i % 2 == 0 ? kalt : keys);
         u32* vout = last ? perm : (i % 2 == 0 ? valt : vtmp);
-        LO_CUDA(cudaMemsetAsync(status, 0, static_cast<size_t>(tiles) * 256 * 8, ctx->stream));
-        LO_CUDA(cudaMemsetAsync(counter, 0, 4, ctx->stream));
+        LO_CUDA(cudaMemsetAsync(counter + i, 0, 4, ctx->stream));
         if (i == 0)
             onesweep_pass<true><<<tiles, kSortThreads, smem, ctx->stream>>>(
-                kin, nullptr, kout, vout, n, 8 * run[i], dbase + 256 * run[i], status, counter);
+                kin, nullptr, kout, vout, n, 8 * run[i], dbase + 256 * run[i], status, counter + i, i + 1);
         else
             onesweep_pass<false><<<tiles, kSortThreads, smem, ctx->stream>>>(
-                kin, vin, kout, vout, n, 8 * run[i], dbase + 256 * run[i], status, counter);
+                kin, vin, kout, vout, n, 8 * run[i], dbase + 256 * run[i], status, counter + i, i + 1);
         LO_CHECK_LAUNCH();
         kin = kout;
         vin = vout;
