@@ -26,11 +26,24 @@ constexpr int kPtWarps = 4;
 #ifndef LO_PT_PREFILTER
 #define LO_PT_PREFILTER 1
 #endif
+// LO_PT_STREAM=1: the walk queues up to 32 kept leaves and streams their points 32 at a time across
+// leaf boundaries, the next 32 prefetched by cp.async while the current ones are filtered.  Measured
+// slower (cfg3 count 33.8 -> 35.5 ms, cfg1 r = 3 4.98 -> 5.23 ms): the stream lookup costs more than
+// the per-leaf load latency it hides.
+#ifndef LO_PT_STREAM
+#define LO_PT_STREAM 0
+#endif
 constexpr int kPtThreads = 32 * kPtWarps;
 
 struct PtShared {
     u32 stack[kStackCap];
-    float4 buf[32];      // candidate (x, y, z) relative FP32, .w = point index bits
+#if LO_PT_STREAM
+    u32 lbeg[32];        // queued leaves (walk order): first point, point count, wanting queries
+    u32 lsize[32];
+    u32 lwant[32];
+    float4 pre[2][32];   // streamed candidate points (FP32, cloud frame), double-buffered
+#endif
+    float tbox[6];       // the tile's FP32 query box (lo xyz, hi xyz)
     u32 bix[32];         // candidate point indices, staged per leaf (loaded per buffer)
     float4 qf[32];       // queries, FP32 relative to the cloud origin (walk: node-box tests)
     // queries, FP32 relative to the tile origin (point tests), SoA: (q[2p], q[2p+1]) loads as
@@ -622,13 +635,13 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
         // the whole tile's query box: candidate points farther than r from it are members of no
         // query of the tile (tile_disjoint_f with the point as a degenerate box), so they are
         // dropped before they take a buffer slot
-        float tl[3], th[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            tl[a] = fminf(gl[a], __shfl_xor_sync(~0u, gl[a], 8));
-            th[a] = fmaxf(gh[a], __shfl_xor_sync(~0u, gh[a], 8));
-            tl[a] = fminf(tl[a], __shfl_xor_sync(~0u, tl[a], 16));
-            th[a] = fmaxf(th[a], __shfl_xor_sync(~0u, th[a], 16));
+            float tl = fminf(gl[a], __shfl_xor_sync(~0u, gl[a], 8));
+            float th = fmaxf(gh[a], __shfl_xor_sync(~0u, gh[a], 8));
+            tl = fminf(tl, __shfl_xor_sync(~0u, tl, 16));
+            th = fmaxf(th, __shfl_xor_sync(~0u, th, 16));
+            if (lane == 0) S.tbox[a] = tl, S.tbox[3 + a] = th;
         }
         u32 fill = 0, qmask = 0;  // buffer occupancy and interested queries (warp-uniform)
         u32 nrec = 0;             // count pass: buffers recorded for the replay
@@ -640,8 +653,10 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             float4 P = make_float4(INFINITY, INFINITY, INFINITY, 0.f);
             if (static_cast<u32>(lane) < fill) {
                 const u32 g = S.bix[lane];
-                P = make_float4(__double2float_rn(__ldg(px + g) - ox), __double2float_rn(__ldg(py + g) - oy),
-                                __double2float_rn(__ldg(pz + g) - oz), __uint_as_float(g));
+                // tile origin = query 0, re-read from shared memory (registers are the limit)
+                P = make_float4(__double2float_rn(__ldg(px + g) - S.qd[0][0]),
+                                __double2float_rn(__ldg(py + g) - S.qd[0][1]),
+                                __double2float_rn(__ldg(pz + g) - S.qd[0][2]), __uint_as_float(g));
             }
             u32 mymask = 0;
             process_buffer<SHAPE, FILL>(S, P, fill, qmask, lane, lo_thr, hi_thr, px, py, pz, r, r2,
@@ -665,6 +680,97 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
                 }
             }
         };
+#if LO_PT_STREAM
+        // The walk queues the leaves it keeps (up to 32); drain() streams their points 32 at a time
+        // across leaf boundaries -- lane j takes stream position s0 + j, its leaf found by a popcount
+        // over the leaves' start positions -- with the next 32 points' loads in flight while the
+        // current ones are filtered against the tile box and appended to the buffer.
+        u32 nl = 0;
+        auto drain = [&]() {
+            __syncwarp();
+            const u32 sz = static_cast<u32>(lane) < nl ? S.lsize[lane] : 0u;
+            u32 inc = sz;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 t = __shfl_up_sync(~0u, inc, o);
+                if (lane >= o) inc += t;
+            }
+            const u32 total = __shfl_sync(~0u, inc, 31);
+            // leaf `lane`'s stream start replaces its size; the rest of the lookup goes through
+            // shared memory (registers are the kernel's limit)
+            const u32 lst = static_cast<u32>(lane) < nl && sz != 0 ? inc - sz : 0xffffffffu;
+            if (static_cast<u32>(lane) < nl) S.lsize[lane] = inc - sz;
+            __syncwarp();
+            const u32 le = (2u << lane) - 1u;  // lanes <= this one (lane 31: all)
+            // point of stream position s0 + lane: index and leaf slot (valid only below total)
+            auto locate = [&](u32 s0, u32& g, u32& j) {
+                const u32 before = __popc(__ballot_sync(~0u, lst < s0));
+                const u32 rel = lst - s0;
+                const u32 B = __reduce_or_sync(~0u, lst != 0xffffffffu && lst >= s0 && rel < 32u ? 1u << rel : 0u);
+                j = (before + __popc(B & le) - 1u) & 31u;
+                g = S.lbeg[j] + (s0 + static_cast<u32>(lane) - S.lsize[j]);
+            };
+            // the next 32 points travel by cp.async straight into this warp's shared slots, so no
+            // registers are held across the buffer flushes
+            u32 g, j;
+            locate(0, g, j);
+            bool valid = static_cast<u32>(lane) < total;
+            const u32 pre0 = static_cast<u32>(__cvta_generic_to_shared(&S.pre[0][lane]));
+            if (valid) asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(pre0), "l"(pf + g) : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            u32 ph = 0;
+            for (u32 s0 = 0; s0 < total; s0 += 32, ph ^= 1u) {
+                u32 g2 = 0, j2 = 0;
+                const bool valid2 = s0 + 32 + static_cast<u32>(lane) < total;
+                if (s0 + 32 < total) {
+                    locate(s0 + 32, g2, j2);
+                    if (valid2)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(pre0 + (ph ^ 1u) * 512u),
+                                     "l"(pf + g2)
+                                     : "memory");
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                } else {
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                }
+                float3 cur = make_float3(0.f, 0.f, 0.f);
+                if (valid) {
+                    const float4 c4 = S.pre[ph][lane];
+                    cur = make_float3(c4.x, c4.y, c4.z);
+                }
+                bool ok = false;
+                if (valid) {
+                    NodeF pt;
+                    pt.lo[0] = pt.hi[0] = cur.x;
+                    pt.lo[1] = pt.hi[1] = cur.y;
+                    pt.lo[2] = pt.hi[2] = cur.z;
+                    ok = !tile_disjoint_f<SHAPE>(S.tbox, S.tbox + 3, pt, ft);
+                }
+                const u32 bal = __ballot_sync(~0u, ok);
+                if (bal) {
+                    const u32 wv = ok ? S.lwant[j] : 0u;
+                    const u32 pos = fill + __popc(bal & ((1u << lane) - 1u));
+                    __syncwarp();
+                    if (ok && pos < 32) S.bix[pos] = g;
+                    qmask |= __reduce_or_sync(~0u, pos < 32 ? wv : 0u);
+                    fill += __popc(bal);
+                    if (fill >= 32) {
+                        const u32 over = fill - 32;
+                        fill = 32;
+                        __syncwarp();
+                        flush();
+                        __syncwarp();
+                        if (ok && pos >= 32) S.bix[pos - 32] = g;
+                        fill = over;
+                        qmask = __reduce_or_sync(~0u, pos >= 32 ? wv : 0u);
+                    }
+                }
+                g = g2, j = j2, valid = valid2;
+            }
+            nl = 0;
+            __syncwarp();
+        };
+#endif
         int sp = 1;
         if (lane == 0) S.stack[0] = 0;
         __syncwarp();
@@ -695,6 +801,15 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             // leaf: which queries can reach it
             const u32 want = __ballot_sync(~0u, active && !disjoint_f<SHAPE>(qf, nd, ft));
             if (!want) continue;
+#if LO_PT_STREAM
+            if (lane == 0) {
+                S.lbeg[nl] = nd.begin;
+                S.lsize[nl] = nd.end - nd.begin;
+                S.lwant[nl] = want;
+            }
+            if (++nl == 32) drain();
+            continue;
+#endif
 #if LO_PT_PREFILTER
             for (u32 b0 = nd.begin; b0 < nd.end; b0 += 32) {
                 const u32 g = b0 + static_cast<u32>(lane);
@@ -705,7 +820,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
                     pt.lo[0] = pt.hi[0] = pp.x;
                     pt.lo[1] = pt.hi[1] = pp.y;
                     pt.lo[2] = pt.hi[2] = pp.z;
-                    ok = !tile_disjoint_f<SHAPE>(tl, th, pt, ft);
+                    ok = !tile_disjoint_f<SHAPE>(S.tbox, S.tbox + 3, pt, ft);
                 }
                 const u32 bal = __ballot_sync(~0u, ok);
                 if (!bal) continue;
@@ -742,6 +857,9 @@ __global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
             }
 #endif
         }
+#if LO_PT_STREAM
+        if (nl) drain();
+#endif
         if (fill) {
             __syncwarp();
             flush();  // partial last buffer

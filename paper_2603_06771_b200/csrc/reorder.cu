@@ -158,9 +158,10 @@ __global__ void __launch_bounds__(256) encode_kernel(const double* __restrict__ 
 // serves every pass.  Order inside a tile: (1) ranking, (2) local offsets and the tile's
 // aggregate published, (3) the tile is scattered into shared memory and its values loaded,
 // (4) only then the look-back for the global digit prefix (predecessors had the scatter's time to
-// publish), (5) coalesced global writes.  cfg3 sort 9.04 -> 7.46 ms, cfg1 1.124 -> 1.027 ms
-// (torch.sort / CUB SortPairs on the same counts of 64-bit keys: 8.61 / 1.03 ms,
-// profiles/r3/sort_v2.log).  LO_SORT_EARLY=1 publishes an early block histogram (shared
+// publish), (5) coalesced global writes.  The look-back reads LO_SORT_LB = 4 predecessors per
+// L2 round trip.  cfg3 sort 9.04 -> 6.62 ms, cfg1 1.124 -> 0.966 ms (torch.sort / CUB SortPairs
+// on the same counts of 64-bit keys: 8.61 / 1.03 ms; profiles/r3/sort_v2.log, sort_lookback.log;
+// one predecessor per round trip: 7.77 / 1.046 ms, eight: 6.66 / 0.974 ms).  LO_SORT_EARLY=1 publishes an early block histogram (shared
 // atomics) before the ranking instead; measured slower (8.09 / 1.073 ms).
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
@@ -175,6 +176,9 @@ constexpr int kSortWarps = kSortThreads / 32;
 #endif
 #ifndef LO_SORT_GROUP
 #define LO_SORT_GROUP 4
+#endif
+#ifndef LO_SORT_LB
+#define LO_SORT_LB 4
 #endif
 constexpr int kSortItems = LO_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;
@@ -197,7 +201,8 @@ template <bool FIRST>
 __global__ void __launch_bounds__(kSortThreads, LO_SORT_MINB) onesweep_pass(
     const u64* __restrict__ kin, const u32* __restrict__ vin, u64* __restrict__ kout,
     u32* __restrict__ vout, u64 n, int shift, const u64* __restrict__ digit_base,
-    u64* status, u32* counter, u32 epoch) {
+    u64* status_, u32* counter, u32 epoch) {
+    volatile u64* status = status_;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -284,17 +289,31 @@ __global__ void __launch_bounds__(kSortThreads, LO_SORT_MINB) onesweep_pass(
         S.vals[rank[i]] = v;
     }
 
-    // (4) look back for this digit's global prefix
+    // (4) look back for this digit's global prefix, LO_SORT_LB predecessors per round trip (the
+    // walk over predecessors that only published their aggregate is a chain of L2 round trips)
     u64 excl = 0;
     if (tile > 0) {
-        volatile u64* sp = status + static_cast<u64>(tile - 1) * 256 + d;
-        for (;;) {
-            const u64 s = *sp;
-            const u64 f = s & kFlagMask;
-            if (f == 0 || (s & ~kFlagMask) >> kEpochShift != epoch) continue;
-            excl += s & kCountMask;
-            if (f == kFlagInc) break;
-            sp -= 256;
+        constexpr int W = LO_SORT_LB;
+        i64 j = static_cast<i64>(tile) - 1;
+        bool done = false;
+        while (!done) {
+            u64 s[W];
+#pragma unroll
+            for (int u = 0; u < W; ++u)
+                s[u] = j - u >= 0 ? status[static_cast<u64>(j - u) * 256 + d] : (kFlagInc | ep);
+            // status words are read with ld.volatile (above: `status` is accessed through a
+            // volatile pointer); consume them nearest first, retry from the first empty one
+            int u = 0;
+            for (; u < W; ++u) {
+                const u64 f = s[u] & kFlagMask;
+                if (f == 0 || (s[u] & ~kFlagMask) >> kEpochShift != epoch) break;
+                excl += s[u] & kCountMask;
+                if (f == kFlagInc) {
+                    done = true;
+                    break;
+                }
+            }
+            if (!done) j -= u;
         }
         st[d] = kFlagInc | ep | (excl + real);
     }
