@@ -32,7 +32,7 @@ xyz = bench.generate(cfg)
 coded, tree = C.c_void_p(), C.c_void_p()
 _lib.check(L.lo_reorder(ctx.h, xyz.ctypes.data, cfg["n"], cfg["curve"], 21, C.byref(coded)))
 _lib.check(L.lo_octree_build(ctx.h, coded, cfg["n_max"], C.byref(tree)))
-out = {"config": a.config, "n": cfg["n"], "ms": {}, "fps_equal": {}}
+out = {"config": a.config, "lib": os.environ.get("LO_LIB_PATH", "in-tree"), "n": cfg["n"], "ms": {}, "fps_equal": {}}
 ref_fps = {}
 for v in a.variants:
     for key in ("LO_KNN_SELECT", "LO_KNN_WIN", "LO_KNN_CAP"):
@@ -54,6 +54,7 @@ for v in a.variants:
         if k not in ref_fps:
             ref_fps[k] = h
         out["fps_equal"][f"{v}@{k}"] = h == ref_fps[k]
+        out.setdefault("fps_xor", {})[f"{v}@{k}"] = f"{h:016x}"
         out["ms"][f"{v}@{k}"] = [round(t, 2) for t in times]
         sys.stderr.write(f"{v} k={k}: {[round(t, 2) for t in times]} ms\n")
 print(json.dumps(out))
