@@ -335,20 +335,45 @@ __global__ void __launch_bounds__(kSortThreads, LO_SORT_MINB) onesweep_pass(
 
 // ---- K4: gather into SFC order, SoA f64 ---------------------------------------------------
 // Also writes the FP32 filter copy fl32(fl64(p - origin)) (search_common.cuh error bounds).
+#ifndef LO_GATHER_ILP
+#define LO_GATHER_ILP 4
+#endif
+// Each thread keeps LO_GATHER_ILP random record gathers in flight (the perm loads first, then all
+// coordinate loads, then the stores): the source records are scattered 24-byte reads.
 __global__ void __launch_bounds__(256) gather_soa(const double* __restrict__ xyz,
                                                   const u32* __restrict__ perm, u64 n,
                                                   double* __restrict__ x, double* __restrict__ y,
                                                   double* __restrict__ z, float4* __restrict__ pf,
                                                   double ox, double oy, double oz) {
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n;
-         i += (u64)gridDim.x * blockDim.x) {
-        const u64 o = perm[i];
-        const double a = xyz[3 * o], b = xyz[3 * o + 1], c = xyz[3 * o + 2];
-        x[i] = a;
-        y[i] = b;
-        z[i] = c;
-        pf[i] = make_float4(__double2float_rn(a - ox), __double2float_rn(b - oy),
-                            __double2float_rn(c - oz), 0.f);
+    constexpr int U = LO_GATHER_ILP;
+    const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+    for (u64 i0 = blockIdx.x * (u64)blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+        u64 o[U];
+        double a[U], b[U], c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const u64 i = i0 + u * stride;
+            o[u] = i < n ? perm[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (i0 + u * stride < n) {
+                a[u] = xyz[3 * o[u]];
+                b[u] = xyz[3 * o[u] + 1];
+                c[u] = xyz[3 * o[u] + 2];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const u64 i = i0 + u * stride;
+            if (i < n) {
+                x[i] = a[u];
+                y[i] = b[u];
+                z[i] = c[u];
+                pf[i] = make_float4(__double2float_rn(a[u] - ox), __double2float_rn(b[u] - oy),
+                                    __double2float_rn(c[u] - oz), 0.f);
+            }
+        }
     }
 }
 
