@@ -148,11 +148,15 @@ static bool launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
                                                                       static_cast<u64>(ctx->sm_count) * 64)));
     if (float_path(t, c, q, r)) {
         FloatTest ft = make_float_test(r, std::max(c->bmax, q.bmax));
-        // internal nodes of <= 64 points are taken whole: ~40 % fewer node visits for ~25 % more
-        // candidates (cfg1 count r = 3: 6.13 -> 5.04 ms, fill 5.22 -> 5.56 ms; LO_COARSE overrides)
+        // internal nodes of <= 256 points are taken whole: fewer node visits, and the walk's
+        // per-point tile-box prefilter drops the far points of a whole node before they take
+        // buffer slots.  With the prefilter, 256 beats 64 (cfg3 count 33.3 -> 30.2 ms, cfg1 r = 3
+        // 4.95 -> 4.34 ms; 512: 30.5 / 4.37, 1024: 31.8 / 4.75; profiles/r3/walk_knobs*.log).
+        // Before the prefilter 64 was best (cfg1 count r = 3: 6.13 -> 5.04 ms vs 0).  LO_COARSE
+        // overrides.
         static const u32 coarse = [] {
             const char* e = std::getenv("LO_COARSE");
-            return e ? static_cast<u32>(std::strtoul(e, nullptr, 10)) : 64u;
+            return e ? static_cast<u32>(std::strtoul(e, nullptr, 10)) : 256u;
         }();
         ft.coarse = coarse;
         // an 8-query group is tested against a child through its FP32 bounding box when its extent
