@@ -151,7 +151,7 @@ static bool launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
         // internal nodes of <= 256 points are taken whole: fewer node visits, and the walk's
         // per-point tile-box prefilter drops the far points of a whole node before they take
         // buffer slots.  With the prefilter, 256 beats 64 (cfg3 count 33.3 -> 30.2 ms, cfg1 r = 3
-        // 4.95 -> 4.34 ms; 512: 30.5 / 4.37, 1024: 31.8 / 4.75; profiles/r3/walk_knobs*.log).
+        // 4.95 -> 4.34 ms; 512: 30.5 / 4.37, 1024: 31.8 / 4.75; profiles/r2b/walk_knobs*.log).
         // Before the prefilter 64 was best (cfg1 count r = 3: 6.13 -> 5.04 ms vs 0).  LO_COARSE
         // overrides.
         static const u32 coarse = [] {

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(256) encode_kernel(const double* __restrict__ 
 // (4) only then the look-back for the global digit prefix (predecessors had the scatter's time to
 // publish), (5) coalesced global writes.  The look-back reads LO_SORT_LB = 4 predecessors per
 // L2 round trip.  cfg3 sort 9.04 -> 6.62 ms, cfg1 1.124 -> 0.966 ms (torch.sort / CUB SortPairs
-// on the same counts of 64-bit keys: 8.61 / 1.03 ms; profiles/r3/sort_v2.log, sort_lookback.log;
+// on the same counts of 64-bit keys: 8.61 / 1.03 ms; profiles/r2b/sort_v2.log, sort_lookback.log;
 // one predecessor per round trip: 7.77 / 1.046 ms, eight: 6.66 / 0.974 ms).  LO_SORT_EARLY=1 publishes an early block histogram (shared
 // atomics) before the ranking instead; measured slower (8.09 / 1.073 ms).
 constexpr int kSortThreads = 256;

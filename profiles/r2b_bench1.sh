@@ -1,5 +1,5 @@
 #!/bin/bash
-# default bench line after the round-3 sort / radius changes, plus the launch list of one step
+# default bench line after the round-2 second-session sort / radius changes, plus the launch list of one step
 OUT=gpurun_out
 timeout 1500 python bench.py > $OUT/b1.json 2> $OUT/b1.err; echo "bench rc=$?"; tail -3 $OUT/b1.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/b1_launches.csv \

@@ -1,7 +1,7 @@
-"""Round-3 ncu summary: the --set full captures of profiles/r3_final_b.sh (g_*_raw.csv, g_*_hot_lines.txt,
-exported on the box) and the launch list of profiles/r3_final_a.sh, as markdown.
+"""Round-3 ncu summary: the --set full captures of profiles/r2b_final_b.sh (g_*_raw.csv, g_*_hot_lines.txt,
+exported on the box) and the launch list of profiles/r2b_final_a.sh, as markdown.
 
-    python profiles/summarize_r3.py --dir gpurun_out --out profiles/r3_cfg3_ncu.md
+    python profiles/summarize_r2b.py --dir gpurun_out --out profiles/r2b_cfg3_ncu.md
 """
 import argparse
 import os
@@ -23,12 +23,12 @@ CAPS = [
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dir", default="gpurun_out")
-    ap.add_argument("--out", default="profiles/r3_cfg3_ncu.md")
-    ap.add_argument("--launches", default="profiles/r3/launches_cfg3.csv")
+    ap.add_argument("--out", default="profiles/r2b_cfg3_ncu.md")
+    ap.add_argument("--launches", default="profiles/r2b/launches_cfg3.csv")
     a = ap.parse_args()
-    L = ["# ncu summary -- round 3 (cfg3, plus cfg1 count at r = 3 and a cfg1 sort pass)", "",
-         "One B200. `--set full --clock-control none --import-source on` captures by `profiles/r3_final_b.sh`, "
-         "each after the same command exited 0 without ncu; launch list by `profiles/r3_final_a.sh`. ncu times "
+    L = ["# ncu summary -- round 2, second session (cfg3, plus cfg1 count at r = 3 and a cfg1 sort pass)", "",
+         "One B200. `--set full --clock-control none --import-source on` captures by `profiles/r2b_final_b.sh`, "
+         "each after the same command exited 0 without ncu; launch list by `profiles/r2b_final_a.sh`. ncu times "
          "are cold-cache and serialised: compare shares, not absolute times, with the bench line.", ""]
     agg = launch_table(a.launches)
     tot = sum(v[1] for v in agg.values()) or 1.0
