@@ -341,6 +341,21 @@ int lo_structure_copy(lo_context* dst, const lo_coded* coded, const lo_octree* t
 int lo_radius_sharded(lo_comm* comm, const lo_octree* tree, const lo_coded* coded, int method, int shape,
                       double radius, int fingerprint, lo_csr** out, uint64_t* row_begin, uint64_t* row_base,
                       uint64_t* total);
+/* Work-weighted shard bounds (the radius work follows neighbour counts, and cfg3's
+ * cluster rows are ~10x the terrain ones).  lo_weighted_bounds is host arithmetic: sample j stands
+ * for queries [j*stride, min((j+1)*stride, n)) with cost (sample_counts[j] + base_cost) per query;
+ * bounds[0..nranks] (bounds[0] = 0, bounds[nranks] = n, multiples of `stride` in between) split the
+ * cumulative cost evenly.  lo_radius_work_bounds measures them with one radius batch over the first
+ * 32 centres (one query tile) of every stride block -- 32/stride of the work, deterministic, so
+ * every rank computes the same bounds without communication; stride >= 32, a multiple of 32. */
+int lo_weighted_bounds(const uint32_t* sample_counts, uint64_t samples, uint32_t stride, uint64_t n,
+                       uint32_t base_cost, int nranks, uint64_t* bounds);
+int lo_radius_work_bounds(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int shape,
+                          double radius, uint32_t stride, int nranks, uint64_t* bounds);
+/* lo_radius_sharded over the caller's bounds[0..nranks] instead of equal slices. */
+int lo_radius_sharded_bounds(lo_comm* comm, const lo_octree* tree, const lo_coded* coded, int method, int shape,
+                             double radius, int fingerprint, const uint64_t* bounds, lo_csr** out,
+                             uint64_t* row_begin, uint64_t* row_base, uint64_t* total);
 /* run_knn_batch in Full mode over this rank's slice (fixed-width rows: no exchange). */
 int lo_knn_sharded(lo_comm* comm, const lo_octree* tree, const lo_coded* coded, uint32_t k, int fingerprint,
                    lo_knn_result** out, uint64_t* row_begin);

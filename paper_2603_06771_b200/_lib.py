@@ -110,6 +110,9 @@ SIGNATURES = {
     "lo_broadcast_structure": (cint, [P, P, P, cint, PP, PP]),
     "lo_structure_copy": (cint, [P, P, P, PP, PP]),
     "lo_radius_sharded": (cint, [P, P, P, cint, cint, f64, cint, PP, P, P, P]),
+    "lo_weighted_bounds": (cint, [P, u64, u32, u64, u32, cint, P]),
+    "lo_radius_work_bounds": (cint, [P, P, P, cint, f64, u32, cint, P]),
+    "lo_radius_sharded_bounds": (cint, [P, P, P, cint, cint, f64, cint, P, PP, P, P, P]),
     "lo_knn_sharded": (cint, [P, P, P, u32, cint, PP, P]),
     "lo_octant_bounds": (cint, [P, cint, u32, u32, u32, cint, P]),
     "lo_knn_destroy": (cint, [P]),

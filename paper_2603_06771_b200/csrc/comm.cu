@@ -328,15 +328,88 @@ int lo_structure_copy(lo_context* dst, const lo_coded* coded, const lo_octree* t
     });
 }
 
-int lo_radius_sharded(lo_comm* comm, const lo_octree* tree, const lo_coded* coded, int method, int shape,
-                      double radius, int fingerprint, lo_csr** out, uint64_t* row_begin, uint64_t* row_base,
-                      uint64_t* total) {
+int lo_weighted_bounds(const uint32_t* sample_counts, uint64_t samples, uint32_t stride, uint64_t n,
+                       uint32_t base_cost, int nranks, uint64_t* bounds) {
+    return api([&] {
+        require(bounds && nranks >= 1 && stride >= 1, LO_INVALID_ARGUMENT, "weighted_bounds: bad arguments");
+        require(samples == (n + stride - 1) / stride, LO_INVALID_ARGUMENT,
+                "weighted_bounds: one sample per stride block expected");
+        require(samples == 0 || sample_counts, LO_INVALID_ARGUMENT, "weighted_bounds: null counts");
+        // cumulative cost at the end of each stride block (exact in u128 arithmetic)
+        std::vector<unsigned __int128> cum(samples);
+        unsigned __int128 acc = 0;
+        for (u64 j = 0; j < samples; ++j) {
+            const u64 q = std::min<u64>(stride, n - j * stride);
+            acc += static_cast<unsigned __int128>(q) * (static_cast<u64>(sample_counts[j]) + base_cost);
+            cum[j] = acc;
+        }
+        bounds[0] = 0;
+        u64 j = 0;
+        for (int r = 1; r < nranks; ++r) {
+            const unsigned __int128 target = acc * static_cast<unsigned>(r) / static_cast<unsigned>(nranks);
+            while (j < samples && cum[j] <= target) ++j;  // first block whose end passes the target
+            // the bound goes to the nearer block edge
+            u64 cut = j;
+            if (j < samples) {
+                const unsigned __int128 before = j ? cum[j - 1] : 0;
+                if (target - before > cum[j] - target) cut = j + 1;
+            }
+            bounds[r] = std::max(bounds[r - 1], std::min<u64>(n, cut * stride));
+        }
+        bounds[nranks] = n;
+    });
+}
+
+int lo_radius_work_bounds(lo_context* ctx, const lo_octree* tree, const lo_coded* coded, int shape,
+                          double radius, uint32_t stride, int nranks, uint64_t* bounds) {
+    return api_ctx(ctx, [&] {
+        require(tree && coded && bounds, LO_INVALID_ARGUMENT, "null tree, cloud or bounds");
+        require(stride >= 32 && stride % 32 == 0 && nranks >= 1, LO_INVALID_ARGUMENT,
+                "radius_work_bounds: stride must be a positive multiple of 32");
+        // one whole query tile (32 consecutive centres) at the start of every stride block: sampled
+        // tiles stay as compact as the batch's own (every-stride-th centres made each sampled tile
+        // span 32 blocks: 6 ms at cfg3 instead of ~1/64 of the count)
+        const u64 n = coded->n, samples = (n + stride - 1) / stride;
+        std::vector<u32> centres;
+        centres.reserve(samples * 32);
+        for (u64 j = 0; j < samples; ++j)
+            for (u64 i = j * stride; i < std::min<u64>(n, j * stride + 32); ++i) centres.push_back(static_cast<u32>(i));
+        std::vector<u32> rows(centres.size()), counts(samples);
+        lo_csr* csr = nullptr;
+        int rc = lo_radius(ctx, tree, coded, LO_METHOD_LIN, shape, radius, centres.data(), centres.size(), 0, &csr);
+        if (rc != LO_OK) throw Error(rc, lo_last_error());
+        rc = lo_csr_download(ctx, csr, rows.data(), nullptr, nullptr, nullptr);
+        lo_csr_destroy(csr);
+        if (rc != LO_OK) throw Error(rc, lo_last_error());
+        for (u64 j = 0, c = 0; j < samples; ++j) {  // mean neighbours per query of the sampled tile
+            const u64 k = std::min<u64>(32, n - j * stride);
+            u64 sum = 0;
+            for (u64 i = 0; i < k; ++i) sum += rows[c + i];
+            c += k;
+            counts[j] = static_cast<u32>((sum + k / 2) / k);
+        }
+        // per-query fixed cost ~16 neighbour-equivalents (the walk and the tile's buffers)
+        rc = lo_weighted_bounds(counts.data(), samples, stride, n, 16, nranks, bounds);
+        if (rc != LO_OK) throw Error(rc, lo_last_error());
+    });
+}
+
+static int radius_sharded_impl(lo_comm* comm, const lo_octree* tree, const lo_coded* coded, int method, int shape,
+                               double radius, int fingerprint, const uint64_t* bounds, lo_csr** out,
+                               uint64_t* row_begin, uint64_t* row_base, uint64_t* total) {
     if (!comm) return api([] { throw Error(LO_INVALID_ARGUMENT, "null comm"); });
     return api_ctx(comm->ctx, [&] {
         lo_context* ctx = comm->ctx;
         require(tree && coded && out, LO_INVALID_ARGUMENT, "null tree, cloud or output");
         u64 b = 0, e = 0;
-        shard(coded->n, comm->rank, comm->nranks, &b, &e);
+        if (bounds) {
+            b = bounds[comm->rank];
+            e = bounds[comm->rank + 1];
+            require(b <= e && e <= coded->n && bounds[0] == 0 && bounds[comm->nranks] == coded->n,
+                    LO_INVALID_ARGUMENT, "radius_sharded: bounds must cover [0, n) in order");
+        } else {
+            shard(coded->n, comm->rank, comm->nranks, &b, &e);
+        }
         lo_csr* csr = nullptr;
         const int rc = lo_radius_range(ctx, tree, coded, method, shape, radius, b, e, fingerprint, &csr);
         if (rc != LO_OK) throw Error(rc, lo_last_error());
@@ -365,6 +438,21 @@ int lo_radius_sharded(lo_comm* comm, const lo_octree* tree, const lo_coded* code
         if (row_base) *row_base = base;
         if (total) *total = sum;
     });
+}
+
+int lo_radius_sharded(lo_comm* comm, const lo_octree* tree, const lo_coded* coded, int method, int shape,
+                      double radius, int fingerprint, lo_csr** out, uint64_t* row_begin, uint64_t* row_base,
+                      uint64_t* total) {
+    return radius_sharded_impl(comm, tree, coded, method, shape, radius, fingerprint, nullptr, out, row_begin,
+                               row_base, total);
+}
+
+int lo_radius_sharded_bounds(lo_comm* comm, const lo_octree* tree, const lo_coded* coded, int method, int shape,
+                             double radius, int fingerprint, const uint64_t* bounds, lo_csr** out,
+                             uint64_t* row_begin, uint64_t* row_base, uint64_t* total) {
+    if (!bounds) return api([] { throw Error(LO_INVALID_ARGUMENT, "null bounds"); });
+    return radius_sharded_impl(comm, tree, coded, method, shape, radius, fingerprint, bounds, out, row_begin,
+                               row_base, total);
 }
 
 int lo_knn_sharded(lo_comm* comm, const lo_octree* tree, const lo_coded* coded, uint32_t k, int fingerprint,

@@ -171,7 +171,7 @@ static bool launch_radius(lo_context* ctx, int shape, const lo_octree* t, const 
         u64* counter = dalloc_t<u64>(ctx, 1);
         LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
         const int pblocks = static_cast<int>(std::max<u64>(
-            1, std::min<u64>((tiles + kPtWarps - 1) / kPtWarps, static_cast<u64>(ctx->sm_count) * 8)));
+            1, std::min<u64>((tiles + kPtWarps - 1) / kPtWarps, static_cast<u64>(ctx->sm_count) * LO_PT_MINB)));
         const int digest = FILL || !fps ? 0 : (c->n <= (1u << 24) ? 2 : 1);
 #define LO_RADIUS_F(S)                                                                          \
     case S:                                                                                     \

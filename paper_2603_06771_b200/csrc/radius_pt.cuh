@@ -22,7 +22,13 @@
 
 namespace lo {
 
-constexpr int kPtWarps = 4;
+#ifndef LO_PT_WARPS
+#define LO_PT_WARPS 4
+#endif
+#ifndef LO_PT_MINB
+#define LO_PT_MINB 8
+#endif
+constexpr int kPtWarps = LO_PT_WARPS;
 #ifndef LO_PT_PREFILTER
 #define LO_PT_PREFILTER 1
 #endif
@@ -558,7 +564,7 @@ __device__ __forceinline__ TileTest tile_test(double r, double ext) {
 // This replaces a separate pass that re-read every CSR row (25.5 GB at cfg3).  1: u32 indices,
 // 2: indices < 2^24 (five zero bytes fold into one multiply).
 template <int SHAPE, bool FILL, int DIGEST = 0>
-__global__ void __launch_bounds__(kPtThreads, 8) radius_pt_kernel(
+__global__ void __launch_bounds__(kPtThreads, LO_PT_MINB) radius_pt_kernel(
     const TNodeF* __restrict__ tf, const float4* __restrict__ pf, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, Queries q, FloatTest ft,
     float compact, double r, double r2, u32* __restrict__ counts, const u64* __restrict__ offsets,

@@ -168,12 +168,20 @@ class Comm:
         check(_lib.lib().lo_broadcast_structure(self.h, coded_h, tree_h, root, C.byref(c), C.byref(t)))
         return (coded_h, tree_h) if self.rank == root else (c, t)
 
-    def radius(self, tree_h, coded_h, r: float, method: int = 1, shape: int = 0, fingerprint: int = 1):
-        """-> (csr handle, row_begin, row_base, total neighbours of all ranks)"""
+    def radius(self, tree_h, coded_h, r: float, method: int = 1, shape: int = 0, fingerprint: int = 1,
+               bounds: np.ndarray | None = None):
+        """-> (csr handle, row_begin, row_base, total neighbours of all ranks); `bounds` (nranks + 1 u64, e.g.
+        from work_bounds) replaces the equal slices."""
         csr = C.c_void_p()
         b, base, tot = C.c_uint64(), C.c_uint64(), C.c_uint64()
-        check(_lib.lib().lo_radius_sharded(self.h, tree_h, coded_h, method, shape, r, fingerprint, C.byref(csr),
-                                           C.byref(b), C.byref(base), C.byref(tot)))
+        if bounds is None:
+            check(_lib.lib().lo_radius_sharded(self.h, tree_h, coded_h, method, shape, r, fingerprint, C.byref(csr),
+                                               C.byref(b), C.byref(base), C.byref(tot)))
+        else:
+            bd = np.ascontiguousarray(bounds, dtype=np.uint64)
+            check(_lib.lib().lo_radius_sharded_bounds(self.h, tree_h, coded_h, method, shape, r, fingerprint,
+                                                      bd.ctypes.data, C.byref(csr), C.byref(b), C.byref(base),
+                                                      C.byref(tot)))
         return csr, b.value, base.value, tot.value
 
     def knn(self, tree_h, coded_h, k: int, fingerprint: int = 1):
@@ -181,6 +189,24 @@ class Comm:
         b = C.c_uint64()
         check(_lib.lib().lo_knn_sharded(self.h, tree_h, coded_h, k, fingerprint, C.byref(res), C.byref(b)))
         return res, b.value
+
+
+def weighted_bounds(sample_counts: np.ndarray, stride: int, n: int, world: int, base_cost: int = 16) -> np.ndarray:
+    """lo_weighted_bounds (host arithmetic, no device): bounds[0..world] splitting the sampled radius
+    work evenly (sample j covers queries [j*stride, (j+1)*stride), cost count_j + base_cost each)."""
+    c = np.ascontiguousarray(sample_counts, dtype=np.uint32)
+    out = np.zeros(world + 1, dtype=np.uint64)
+    check(_lib.lib().lo_weighted_bounds(c.ctypes.data, len(c), stride, n, base_cost, world, out.ctypes.data))
+    return out
+
+
+def radius_work_bounds(ctx, tree_h, coded_h, r: float, world: int, stride: int = 2048, shape: int = 0) -> np.ndarray:
+    """lo_radius_work_bounds: one radius batch over the first query tile (32 centres) of every stride
+    block, then weighted_bounds on the tiles' mean counts.
+    Deterministic, so every rank computes the same bounds on its own copy of the structure."""
+    out = np.zeros(world + 1, dtype=np.uint64)
+    check(_lib.lib().lo_radius_work_bounds(ctx.h, tree_h, coded_h, shape, r, stride, world, out.ctypes.data))
+    return out
 
 
 def structure_copy(dst_ctx, coded_h, tree_h):

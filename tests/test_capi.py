@@ -90,3 +90,56 @@ def test_shard_range_host():
             assert prev == n
     b, e = C.c_uint64(), C.c_uint64()
     assert L.lo_shard_range(10, 2, 2, C.byref(b), C.byref(e)) == _lib.INVALID_ARGUMENT
+
+
+def _weighted_bounds_ref(counts, stride, n, base, g):
+    """Restatement of lo_weighted_bounds' rule: cut at the block edge nearest to each total*r/g."""
+    import numpy as np
+    q = np.minimum(stride, n - np.arange(len(counts), dtype=np.int64) * stride)
+    cum = np.cumsum(q.astype(object) * (np.asarray(counts, dtype=object) + base))
+    total = int(cum[-1]) if len(cum) else 0
+    out, j = [0], 0
+    for r in range(1, g):
+        t = total * r // g
+        while j < len(cum) and cum[j] <= t:
+            j += 1
+        cut = j
+        if j < len(cum):
+            before = int(cum[j - 1]) if j else 0
+            if t - before > int(cum[j]) - t:
+                cut = j + 1
+        out.append(max(out[-1], min(n, cut * stride)))
+    out.append(n)
+    return out
+
+
+def test_weighted_bounds_host():
+    """lo_weighted_bounds (host arithmetic): covering, ordered, stride-aligned cuts that
+    split the sampled work evenly; equals the restated rule; uniform work gives ~equal slices."""
+    import numpy as np
+    from paper_2603_06771_b200 import distributed as D
+    rng = np.random.default_rng(3)
+    for n, stride in ((1, 64), (1000, 64), (100_000, 64), (1_000_003, 32), (64 * 10, 64)):
+        samples = (n + stride - 1) // stride
+        for kind in ("uniform", "skewed", "zeros"):
+            if kind == "uniform":
+                c = np.full(samples, 50, np.uint32)
+            elif kind == "zeros":
+                c = np.zeros(samples, np.uint32)
+            else:  # a dense cluster in the middle: 10x the work
+                c = rng.integers(20, 80, samples).astype(np.uint32)
+                c[samples // 3: samples // 2] *= 10
+            for g in (1, 2, 3, 8):
+                b = D.weighted_bounds(c, stride, n, g)
+                assert b[0] == 0 and b[-1] == n and np.all(np.diff(b.astype(np.int64)) >= 0)
+                assert all(int(x) % stride == 0 for x in b[1:-1] if int(x) != n)
+                assert [int(x) for x in b] == _weighted_bounds_ref(c, stride, n, 16, g)
+                if samples >= 8 * g:  # each rank within one block's cost of the even share
+                    q = np.minimum(stride, n - np.arange(samples) * stride)
+                    cost = q * (c.astype(np.int64) + 16)
+                    per = [cost[int(b[r]) // stride: (int(b[r + 1]) + stride - 1) // stride].sum() for r in range(g)]
+                    assert max(per) - cost.sum() / g <= cost.max() + 1
+    L = _lib.lib()
+    out = np.zeros(3, np.uint64)
+    c = np.zeros(2, np.uint32)
+    assert L.lo_weighted_bounds(c.ctypes.data, 3, 64, 100, 16, 2, out.ctypes.data) == _lib.INVALID_ARGUMENT

@@ -162,3 +162,55 @@ def test_c_abi_nccl_comm_world_one():
     L.lo_octree_destroy(tree)
     L.lo_coded_destroy(coded)
     comm.close()
+
+
+def test_work_weighted_shards():
+    """§8e.3: lo_radius_work_bounds (a radius batch over one query tile per stride block) gives bounds that cover the
+    cloud, are identical when recomputed (every rank derives them alone), balance the neighbour work
+    of a clustered cloud better than equal slices, and whose slices concatenate to the single batch;
+    lo_radius_sharded_bounds at world size 1 takes them."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a B200")
+    from oracle.oracle_py import Oracle
+    from paper_2603_06771_b200 import _lib, distributed as D, linoct as lo
+    L = _lib.lib()
+    ctx = lo.Context(0)
+    n, r, g = 400_000, 1.0, 8
+    pts = Oracle().gen_mixed(n, 11)
+    coded, tree = C.c_void_p(), C.c_void_p()
+    _lib.check(L.lo_reorder(ctx.h, pts.ctypes.data, n, 1, 21, C.byref(coded)))
+    _lib.check(L.lo_octree_build(ctx.h, coded, 64, C.byref(tree)))
+    bw = D.radius_work_bounds(ctx, tree, coded, r, g, stride=256)
+    assert np.array_equal(bw, D.radius_work_bounds(ctx, tree, coded, r, g, stride=256))
+    assert bw[0] == 0 and bw[-1] == n and np.all(np.diff(bw.astype(np.int64)) >= 0)
+    full = C.c_void_p()
+    _lib.check(L.lo_radius_range(ctx.h, tree, coded, 1, 0, r, 0, n, 1, C.byref(full)))
+    fc, ff, _, fi = _csr_rows(L, ctx.h, full)
+    parts = []
+    for k in range(g):
+        s = C.c_void_p()
+        _lib.check(L.lo_radius_range(ctx.h, tree, coded, 1, 0, r, int(bw[k]), int(bw[k + 1]), 1, C.byref(s)))
+        parts.append(_csr_rows(L, ctx.h, s))
+        L.lo_csr_destroy(s)
+    assert np.array_equal(np.concatenate([p[0] for p in parts]), fc)
+    assert np.array_equal(np.concatenate([p[1] for p in parts]), ff)
+    assert np.array_equal(np.concatenate([p[3] for p in parts]), fi)
+    cum = np.concatenate([[0], np.cumsum(fc.astype(np.int64) + 16)])
+    eq = [D.shard_range(n, k, g) for k in range(g)]
+    imb = lambda bb: max(cum[e] - cum[b] for b, e in bb) / (cum[-1] / g)  # noqa: E731
+    w = imb([(int(bw[k]), int(bw[k + 1])) for k in range(g)])
+    assert w <= 1.05 and w <= imb(eq) + 0.03  # sampled estimate: within a few % of even
+    comm = D.Comm(ctx, 0, 1)
+    b1 = D.radius_work_bounds(ctx, tree, coded, r, 1, stride=256)
+    assert list(b1) == [0, n]
+    csr, b, base, total = comm.radius(tree, coded, r, bounds=b1)
+    assert b == 0 and base == 0 and total == int(fc.astype(np.uint64).sum())
+    for h in (csr, full):
+        L.lo_csr_destroy(h)
+    L.lo_octree_destroy(tree)
+    L.lo_coded_destroy(coded)
+    comm.close()
