@@ -197,6 +197,9 @@ __device__ __forceinline__ void struct_buffer(StructShared& SS, const float4 P, 
     }
 }
 
+#ifndef LO_ST_PREFILTER
+#define LO_ST_PREFILTER 1
+#endif
 // MODE 0: count walk (counts, range / single counts, ranges into per-query scratch slots,
 //         per-buffer records for the singles replay);
 // MODE 2: full fill walk (ranges + singles) over `tile_list` (overflowed tiles) or every tile.
@@ -268,6 +271,17 @@ __global__ void __launch_bounds__(kPtThreads, 8) struct_pt_kernel(
             }
         }
         const bool gcompact = fmaxf(fmaxf(gh[0] - gl[0], gh[1] - gl[1]), gh[2] - gl[2]) <= compact;
+#if LO_ST_PREFILTER
+        // the whole tile's query box for the leaf-point prefilter (as in the lin walk)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            float tl = fminf(gl[a], __shfl_xor_sync(~0u, gl[a], 8));
+            float th = fmaxf(gh[a], __shfl_xor_sync(~0u, gh[a], 8));
+            tl = fminf(tl, __shfl_xor_sync(~0u, tl, 16));
+            th = fmaxf(th, __shfl_xor_sync(~0u, th, 16));
+            if (lane == 0) S.tbox[a] = tl, S.tbox[3 + a] = th;
+        }
+#endif
         u32 fill = 0, qmask = 0, nrec = 0;
         u32* rec_tile = (MODE == 0 && rp.pool && chunk_left >= rp.cap) ? rp.pool + chunk_base * 64 : nullptr;
         auto flush = [&]() {
@@ -349,6 +363,39 @@ __global__ void __launch_bounds__(kPtThreads, 8) struct_pt_kernel(
                 continue;
             }
             // leaf: its points, wanted by the lanes that found it Intersects
+#if LO_ST_PREFILTER
+            // a point farther than r from the tile's query box is a single of no tile query: dropped
+            // before it takes a buffer slot (survivors keep point order, so singles stay ascending)
+            for (u32 b0 = nd.begin; b0 < nd.end; b0 += 32) {
+                const u32 g = b0 + static_cast<u32>(lane);
+                bool ok = false;
+                if (g < nd.end) {
+                    const float4 pp = __ldg(pf + g);
+                    NodeF pt;
+                    pt.lo[0] = pt.hi[0] = pp.x;
+                    pt.lo[1] = pt.hi[1] = pp.y;
+                    pt.lo[2] = pt.hi[2] = pp.z;
+                    ok = !tile_disjoint_f<SHAPE>(S.tbox, S.tbox + 3, pt, ft);
+                }
+                const u32 bal = __ballot_sync(~0u, ok);
+                if (!bal) continue;
+                const u32 pos = fill + __popc(bal & ((1u << lane) - 1u));
+                __syncwarp();
+                if (ok && pos < 32) S.bix[pos] = g, SS.sw[pos] = inter;
+                fill += __popc(bal);
+                qmask |= inter;
+                if (fill >= 32) {
+                    const u32 over = fill - 32;
+                    fill = 32;
+                    __syncwarp();
+                    flush();
+                    __syncwarp();
+                    if (ok && pos >= 32) S.bix[pos - 32] = g, SS.sw[pos - 32] = inter;
+                    fill = over;
+                    qmask = over ? inter : 0u;
+                }
+            }
+#else
             for (u32 base = nd.begin; base < nd.end;) {
                 const u32 take = min(32u - fill, nd.end - base);
                 __syncwarp();
@@ -366,6 +413,7 @@ __global__ void __launch_bounds__(kPtThreads, 8) struct_pt_kernel(
                     qmask = 0;
                 }
             }
+#endif
         }
         if (fill) {
             __syncwarp();
