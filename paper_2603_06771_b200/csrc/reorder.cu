@@ -338,6 +338,19 @@ __global__ void __launch_bounds__(kSortThreads, LO_SORT_MINB) onesweep_pass(
 #ifndef LO_GATHER_ILP
 #define LO_GATHER_ILP 4
 #endif
+// The scattered 24-byte record reads of the gather, with the L2 fetch size cut to 64 bytes: the
+// default fetched 128 per miss, ~145 B of DRAM reads per record (cfg3 gather: 14.5 -> 8.3 GB of
+// DRAM reads, 3.45 -> 3.38 ms).  The L1 keeps allocating: x, y, z of a record share its sector
+// (L1::no_allocate measured 6.4 ms).  LO_GATHER_PLAIN=1: plain loads.
+__device__ __forceinline__ double gather_ld(const double* p) {
+#if LO_GATHER_PLAIN
+    return *p;
+#else
+    double v;
+    asm volatile("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#endif
+}
 // Each thread keeps LO_GATHER_ILP random record gathers in flight (the perm loads first, then all
 // coordinate loads, then the stores): the source records are scattered 24-byte reads.
 __global__ void __launch_bounds__(256) gather_soa(const double* __restrict__ xyz,
@@ -358,9 +371,9 @@ __global__ void __launch_bounds__(256) gather_soa(const double* __restrict__ xyz
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (i0 + u * stride < n) {
-                a[u] = xyz[3 * o[u]];
-                b[u] = xyz[3 * o[u] + 1];
-                c[u] = xyz[3 * o[u] + 2];
+                a[u] = gather_ld(xyz + 3 * o[u]);
+                b[u] = gather_ld(xyz + 3 * o[u] + 1);
+                c[u] = gather_ld(xyz + 3 * o[u] + 2);
             }
         }
 #pragma unroll

@@ -1,0 +1,11 @@
+#!/bin/bash
+# gather record-load variants: time (sort_probe) and DRAM bytes of gather_soa (ncu)
+OUT=gpurun_out
+for v in in-tree ld1 ld2 ld3 ld4; do
+  if [ $v = in-tree ]; then E=""; else E="LO_LIB_PATH=$PWD/_var/$v/liblinoct_b200.so"; fi
+  env $E timeout 300 python profiles/sort_probe.py --config cfg3 >> $OUT/p23_sort.log 2>&1
+  env $E timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:gather_soa -c 1 --csv \
+     python profiles/sort_probe.py --config cfg3 --reps 0 2>/dev/null | grep -E "dram__bytes|gpu__time" | sed "s/^/$v /" >> $OUT/p23_ncu.log
+done
+cat $OUT/p23_sort.log; cat $OUT/p23_ncu.log | cut -c1-250
+exit 0
