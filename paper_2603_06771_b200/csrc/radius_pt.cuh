@@ -95,14 +95,14 @@ __device__ __forceinline__ void process_buffer(PtShared& S, const float4 P, u32 
     const u32 lo_bits = __float_as_uint(lo_thr);
     const u32 band_bits = __float_as_uint(hi_thr) - lo_bits;
     if (!FILL && kPacked) {
-        // count pass: four queries (two packed pairs) per iteration -- one band vote, one
-        // 16-byte mask store and one loop step for four membership ballots
-        u32 qm = (qmask | (qmask >> 1) | (qmask >> 2) | (qmask >> 3)) & 0x11111111u;
+        // count pass: four queries (two packed pairs) per iteration -- one 16-byte mask store and one
+        // loop step for four membership ballots.  The FP32 band is only tracked per lane in the loop
+        // (min over its values of bits(v) - bits(lo)); one vote after the loop decides whether any
+        // pair fell in the band, and only then are the quads redone with the exact FP64 decisions.
+        const u32 qm0 = (qmask | (qmask >> 1) | (qmask >> 2) | (qmask >> 3)) & 0x11111111u;
         S.msk[lane] = 0u;
         __syncwarp();
-        while (qm) {
-            const int b = __ffs(qm) - 1;  // = 4q
-            qm &= qm - 1;
+        auto quad = [&](int b, float* v) {
             const float4 X = *reinterpret_cast<const float4*>(&S.qx[b]);
             const float4 Y = *reinterpret_cast<const float4*>(&S.qy[b]);
             const u64 dxa = fsub2(PX, pack2(X.x, X.y)), dxb = fsub2(PX, pack2(X.z, X.w));
@@ -116,22 +116,36 @@ __device__ __forceinline__ void process_buffer(PtShared& S, const float4 P, u32 
                 da = ffma2(dza, dza, da);
                 db = ffma2(dzb, dzb, db);
             }
-            float v[4];
             unpack2(da, v[0], v[1]);
             unpack2(db, v[2], v[3]);
+        };
+        u32 band_min = 0xffffffffu;
+        for (u32 qm = qm0; qm; qm &= qm - 1) {
+            const int b = __ffs(qm) - 1;  // = 4q
+            float v[4];
+            quad(b, v);
             u32 in[4];
 #pragma unroll
             for (int t = 0; t < 4; ++t) in[t] = __ballot_sync(~0u, v[t] < lo_thr);
             const u32 w01 = min(__float_as_uint(v[0]) - lo_bits, __float_as_uint(v[1]) - lo_bits);
             const u32 w23 = min(__float_as_uint(v[2]) - lo_bits, __float_as_uint(v[3]) - lo_bits);
-            if (__any_sync(~0u, min(w01, w23) < band_bits)) {  // rare: band points, FP64 decides
+            band_min = min(band_min, min(w01, w23));
+            if (lane == 0) *reinterpret_cast<uint4*>(&S.msk[b]) = make_uint4(in[0], in[1], in[2], in[3]);
+        }
+        if (__any_sync(~0u, band_min < band_bits)) {  // rare: band points, exact FP64 decides
+            for (u32 qm = qm0; qm; qm &= qm - 1) {
+                const int b = __ffs(qm) - 1;
+                float v[4];
+                quad(b, v);
+                u32 in[4];
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
+                    in[t] = __ballot_sync(~0u, v[t] < lo_thr);
                     const u32 h = __ballot_sync(~0u, v[t] < hi_thr);
                     if (h ^ in[t]) in[t] = band_fix<SHAPE>(in[t], h ^ in[t], S, b + t, lane, idx, px, py, pz, r, r2);
                 }
+                if (lane == 0) *reinterpret_cast<uint4*>(&S.msk[b]) = make_uint4(in[0], in[1], in[2], in[3]);
             }
-            if (lane == 0) *reinterpret_cast<uint4*>(&S.msk[b]) = make_uint4(in[0], in[1], in[2], in[3]);
         }
         __syncwarp();
         mymask = S.msk[lane];
