@@ -39,6 +39,9 @@ constexpr int kPtWarps = LO_PT_WARPS;
 #ifndef LO_PT_STREAM
 #define LO_PT_STREAM 0
 #endif
+#ifndef LO_PT_UNROLL_FULL
+#define LO_PT_UNROLL_FULL 1
+#endif
 constexpr int kPtThreads = 32 * kPtWarps;
 
 struct PtShared {
@@ -120,8 +123,7 @@ __device__ __forceinline__ void process_buffer(PtShared& S, const float4 P, u32 
             unpack2(db, v[2], v[3]);
         };
         u32 band_min = 0xffffffffu;
-        for (u32 qm = qm0; qm; qm &= qm - 1) {
-            const int b = __ffs(qm) - 1;  // = 4q
+        auto quad_pass = [&](int b) {
             float v[4];
             quad(b, v);
             u32 in[4];
@@ -131,6 +133,15 @@ __device__ __forceinline__ void process_buffer(PtShared& S, const float4 P, u32 
             const u32 w23 = min(__float_as_uint(v[2]) - lo_bits, __float_as_uint(v[3]) - lo_bits);
             band_min = min(band_min, min(w01, w23));
             if (lane == 0) *reinterpret_cast<uint4*>(&S.msk[b]) = make_uint4(in[0], in[1], in[2], in[3]);
+        };
+#if LO_PT_UNROLL_FULL
+        if (qm0 == 0x11111111u) {  // every query interested (the common case): straight-line, static offsets
+#pragma unroll
+            for (int q = 0; q < 8; ++q) quad_pass(4 * q);
+        } else
+#endif
+        {
+            for (u32 qm = qm0; qm; qm &= qm - 1) quad_pass(__ffs(qm) - 1);  // b = 4q
         }
         if (__any_sync(~0u, band_min < band_bits)) {  // rare: band points, exact FP64 decides
             for (u32 qm = qm0; qm; qm &= qm - 1) {
