@@ -3,7 +3,7 @@
 NCU="ncu --set full --clock-control none --import-source on"
 cap() {
   local name=$1 re=$2 extra=$3; shift 3
-  timeout 900 $NCU -k regex:"$re" $extra -o /tmp/$name "$@" > gpurun_out/ncu_$name.log 2>&1
+  timeout 900 $NCU -f -k regex:"$re" $extra -o /tmp/$name "$@" > gpurun_out/ncu_$name.log 2>&1
   ncu -i /tmp/$name.ncu-rep --page raw --csv > gpurun_out/${name}_raw.csv 2>/dev/null
   ncu -i /tmp/$name.ncu-rep --page source --csv --print-source cuda,sass > /tmp/${name}_src.csv 2>/dev/null
   python - "$name" <<'PY'
