@@ -329,6 +329,9 @@ __device__ __forceinline__ void knn_stage_idx(const KnnSmem& S, const float4* __
     __syncwarp();
 }
 
+#ifndef LO_KNN_PREFILTER_MIN_K
+#define LO_KNN_PREFILTER_MIN_K 9
+#endif
 constexpr int kKnnFloatStack = kStackCap;
 constexpr i64 kSeedSortedIdx = -2;  // seed_base: queries are ascending cloud indices (q.idx)
 
@@ -444,12 +447,43 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
         // 2) octree walk; a node is entered if some query's threshold reaches its box
         u32 kfill = 0;
         bool kwant = false;
+        // Point prefilter for the gathered leaves (as in the radius walk; k >= 16 -- k = 8's thresholds
+        // are tight enough that the filter costs more, 6.77 -> 7.07 ms at cfg1; k = 16: cfg3 149.7 ->
+        // 144.5 ms, cfg1 11.93 -> 11.82 ms): a candidate whose FP32 squared distance to the tile's
+        // query box exceeds every lane's threshold T would be rejected by every lane (each lane's
+        // d2 >= the box value: per axis |p - q| >= the gap and the FP32 ops are monotone), so it is
+        // dropped before it takes a slot.  max_t is a stale upper bound of the lanes' T (T only
+        // decreases), refreshed after each flush.
+        constexpr bool KPF = !KEYED && KC >= LO_KNN_PREFILTER_MIN_K;
+        float tb[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        auto warp_max_t = [&]() {
+            float m = T;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(~0u, m, o));
+            return m;
+        };
+        float max_t = INFINITY;
+        if constexpr (KPF) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const float c = a == 0 ? qf.x : (a == 1 ? qf.y : qf.z);
+                float lo_ = c, hi_ = c;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    lo_ = fminf(lo_, __shfl_xor_sync(~0u, lo_, o));
+                    hi_ = fmaxf(hi_, __shfl_xor_sync(~0u, hi_, o));
+                }
+                tb[a] = lo_, tb[3 + a] = hi_;
+            }
+            max_t = warp_max_t();
+        }
         auto kflush = [&]() {
             knn_stage_idx(S, pf, px, py, pz, kfill, lane);
             knn_chunk<KC>(S, kfill, kwant, QX, QY, QZ, heap, k, worst_d, worst_i, T, E, cx, cy, cz, skip_lo,
                           skip_hi);
             kfill = 0;
             kwant = false;
+            if constexpr (KPF) max_t = warp_max_t();
         };
         int sp = 1;
         if (lane == 0) S.stack[0] = 0;
@@ -503,6 +537,36 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
                 // gather the leaf's indices; 32 of them (from several small leaves) are staged and
                 // offered at once -- one load latency per 32 candidates instead of one per leaf
                 // (k = 8: 6.98 -> 6.55 ms, k = 16: 11.17 -> 11.03 ms at cfg1)
+                if constexpr (KPF) {
+                for (u32 b0 = nd.begin; b0 < nd.end; b0 += 32) {
+                    const u32 g = b0 + static_cast<u32>(lane);
+                    bool ok = false;
+                    if (g < nd.end) {
+                        const float4 pp = __ldg(pf + g);
+                        const float gx = fmaxf(fmaxf(tb[0] - pp.x, pp.x - tb[3]), 0.f);
+                        const float gy = fmaxf(fmaxf(tb[1] - pp.y, pp.y - tb[4]), 0.f);
+                        const float gz = fmaxf(fmaxf(tb[2] - pp.z, pp.z - tb[5]), 0.f);
+                        ok = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx))) <= max_t;
+                    }
+                    const u32 bal = __ballot_sync(~0u, ok);
+                    if (!bal) continue;
+                    const u32 pos = kfill + __popc(bal & ((1u << lane) - 1u));
+                    __syncwarp();
+                    if (ok && pos < 32) S.sidx[pos] = g;
+                    kfill += __popc(bal);
+                    kwant |= want;
+                    if (kfill >= 32) {
+                        const u32 over = kfill - 32;
+                        kfill = 32;
+                        __syncwarp();
+                        kflush();
+                        __syncwarp();
+                        if (ok && pos >= 32) S.sidx[pos - 32] = g;
+                        kfill = over;
+                        kwant = over ? want : false;
+                    }
+                }
+                } else {
                 for (u32 b = nd.begin; b < nd.end;) {
                     const u32 take = min(32u - kfill, nd.end - b);
                     __syncwarp();
@@ -511,6 +575,7 @@ __global__ void __launch_bounds__(128) knn_float_kernel(
                     kwant |= want;
                     b += take;
                     if (kfill == 32) kflush();
+                }
                 }
             }
         }
