@@ -598,8 +598,10 @@ void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int lev
     }
     u64* status = dalloc_t<u64>(ctx, static_cast<size_t>(tiles) * 256);
     u32* counter = dalloc_t<u32>(ctx, 8);
-    // one status memset per sort: each pass tags its words with its own epoch (i + 1)
+    // one status memset per sort: each pass tags its words with its own epoch (i + 1); one memset for
+    // the passes' tile counters too
     LO_CUDA(cudaMemsetAsync(status, 0, static_cast<size_t>(tiles) * 256 * 8, ctx->stream));
+    LO_CUDA(cudaMemsetAsync(counter, 0, 8 * sizeof(u32), ctx->stream));
     u64* kalt = dalloc_t<u64>(ctx, n);
     u32* valt = dalloc_t<u32>(ctx, n);
     u32* vtmp = dalloc_t<u32>(ctx, n);
@@ -618,7 +620,6 @@ void radix_sort(lo_context* ctx, u64* keys, u64 n, const u32* hist_host, int lev
         const bool last = i == np - 1;
         u64* kout = last ? keys_sorted : (i % 2 == 0 ? kalt : keys);
         u32* vout = last ? perm : (i % 2 == 0 ? valt : vtmp);
-        LO_CUDA(cudaMemsetAsync(counter + i, 0, 4, ctx->stream));
         if (i == 0)
             onesweep_pass<true><<<tiles, kSortThreads, smem, ctx->stream>>>(
                 kin, nullptr, kout, vout, n, 8 * run[i], dbase + 256 * run[i], status, counter + i, i + 1);
