@@ -25,8 +25,12 @@ namespace lo {
 #ifndef LO_PT_WARPS
 #define LO_PT_WARPS 4
 #endif
+// count-kernel blocks per SM (__launch_bounds__ minimum; the persistent grid is sm_count x this).
+// 10 (48 registers, a 44-byte spill) beats 6 / 7 / 8 / 9 / 12 on cfg1, cfg3 and cfg4: the walk is
+// latency bound and the extra resident warps hide more of it than the spill costs
+// (cfg3 count 30.8 / 30.3 / 28.9 / 28.1 / 27.2 / 29.1 ms, profiles/r3/count_minb_ab.log).
 #ifndef LO_PT_MINB
-#define LO_PT_MINB 8
+#define LO_PT_MINB 10
 #endif
 constexpr int kPtWarps = LO_PT_WARPS;
 #ifndef LO_PT_PREFILTER

@@ -204,7 +204,10 @@ __device__ __forceinline__ void struct_buffer(StructShared& SS, const float4 P, 
 //         per-buffer records for the singles replay);
 // MODE 2: full fill walk (ranges + singles) over `tile_list` (overflowed tiles) or every tile.
 template <int SHAPE, int MODE>
-__global__ void __launch_bounds__(kPtThreads, 8) struct_pt_kernel(
+#ifndef LO_STRUCT_MINB
+#define LO_STRUCT_MINB 8
+#endif
+__global__ void __launch_bounds__(kPtThreads, LO_STRUCT_MINB) struct_pt_kernel(
     const TNodeF* __restrict__ tf, const float4* __restrict__ rbf, const double* __restrict__ rb,
     const float4* __restrict__ pf, const double* __restrict__ px, const double* __restrict__ py,
     const double* __restrict__ pz, Queries q, FloatTest ft, float compact, double r, double r2,
@@ -589,7 +592,7 @@ static void launch_struct_pt(lo_context* ctx, int shape, const lo_octree* t, con
     u64* counter = dalloc_t<u64>(ctx, 1);
     LO_CUDA(cudaMemsetAsync(counter, 0, 8, ctx->stream));
     const int pblocks = static_cast<int>(std::max<u64>(
-        1, std::min<u64>((tiles + kPtWarps - 1) / kPtWarps, static_cast<u64>(ctx->sm_count) * 8)));
+        1, std::min<u64>((tiles + kPtWarps - 1) / kPtWarps, static_cast<u64>(ctx->sm_count) * LO_STRUCT_MINB)));
     static const double compact_mul = [] {  // as in the Lin walk (radius.cu)
         const char* e = std::getenv("LO_COMPACT_MUL");
         return e ? std::strtod(e, nullptr) : 8.0;

@@ -470,6 +470,15 @@ __global__ void decode_codes_kernel(const u64* __restrict__ codes, u64 n, int le
     }
 }
 
+// encode blocks per SM (A/B knob LO_ENCODE_PER_SM; 33 KB of shared memory each, at most 6 resident;
+// 8 measured best: cfg3 encode 1.21 / 1.19 / 1.16 / 1.11 ms at 4 / 5 / 6 / 8, profiles/r3/encode_ab.log)
+static int encode_per_sm() {
+    static const int v = [] {
+        const char* e = std::getenv("LO_ENCODE_PER_SM");
+        return e ? std::max(1, std::atoi(e)) : 8;
+    }();
+    return v;
+}
 static int grid_for(lo_context* ctx, u64 n, int threads, int per_sm = 8) {
     const u64 want = (n + threads - 1) / threads;
     const u64 cap = static_cast<u64>(ctx->sm_count) * per_sm;
@@ -716,7 +725,7 @@ lo_coded* reorder_device(lo_context* ctx, const double* xyz, u64 n, int curve, i
         u32* hist = dalloc_t<u32>(ctx, 8 * 256 + 1);
         LO_CUDA(cudaMemsetAsync(hist, 0, (8 * 256 + 1) * 4, ctx->stream));
         const EncodeParams p = make_params(ctx, disc.box, disc.scale, level, curve);
-        encode_kernel<true><<<grid_for(ctx, n, 256, 4), 256, 0, ctx->stream>>>(
+        encode_kernel<true><<<grid_for(ctx, n, 256, encode_per_sm()), 256, 0, ctx->stream>>>(
             xyz, n, p, codes, hist, hist + 8 * 256);
         LO_CHECK_LAUNCH();
         stage_end(ctx);
@@ -787,7 +796,7 @@ int lo_compute_codes(lo_context* ctx, const double* xyz_host, uint64_t n, int cu
             std::memcpy(scale, d.scale, sizeof scale);
         }
         const EncodeParams p = make_params(ctx, box, scale, level, curve);
-        encode_kernel<false><<<grid_for(ctx, n, 256, 4), 256, 0, ctx->stream>>>(xyz, n, p, codes,
+        encode_kernel<false><<<grid_for(ctx, n, 256, encode_per_sm()), 256, 0, ctx->stream>>>(xyz, n, p, codes,
                                                                                 nullptr, err);
         LO_CHECK_LAUNCH();
         LO_CUDA(cudaMemcpyAsync(codes_host, codes, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
