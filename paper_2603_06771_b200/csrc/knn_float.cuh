@@ -335,8 +335,15 @@ __device__ __forceinline__ void knn_stage_idx(const KnnSmem& S, const float4* __
 constexpr int kKnnFloatStack = kStackCap;
 constexpr i64 kSeedSortedIdx = -2;  // seed_base: queries are ascending cloud indices (q.idx)
 
+// -DLO_KNN_MINB=n sizes the register allocation for n resident blocks per SM (__launch_bounds__
+// minimum); undefined leaves it to ptxas (80 registers at k = 16: 6 blocks of 4 warps per SM).
+#ifdef LO_KNN_MINB
+#define LO_KNN_BOUNDS __launch_bounds__(128, LO_KNN_MINB)
+#else
+#define LO_KNN_BOUNDS __launch_bounds__(128)
+#endif
 template <bool GLOBAL_HEAP, int KC, bool KEYED>
-__global__ void __launch_bounds__(128) knn_float_kernel(
+__global__ void LO_KNN_BOUNDS knn_float_kernel(
     const TNodeF* __restrict__ tf, const float4* __restrict__ pf, const double* __restrict__ px,
     const double* __restrict__ py, const double* __restrict__ pz, u64 npoints, Queries q,
     i64 seed_base, u32 seed_half, float E, u32 k_in, u32* __restrict__ out_idx,
