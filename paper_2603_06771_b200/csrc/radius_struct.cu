@@ -205,7 +205,7 @@ __device__ __forceinline__ void struct_buffer(StructShared& SS, const float4 P, 
 // MODE 2: full fill walk (ranges + singles) over `tile_list` (overflowed tiles) or every tile.
 template <int SHAPE, int MODE>
 #ifndef LO_STRUCT_MINB
-#define LO_STRUCT_MINB 8
+#define LO_STRUCT_MINB 10
 #endif
 __global__ void __launch_bounds__(kPtThreads, LO_STRUCT_MINB) struct_pt_kernel(
     const TNodeF* __restrict__ tf, const float4* __restrict__ rbf, const double* __restrict__ rb,
